@@ -1,0 +1,213 @@
+/*
+ * geot.h — C ABI of the B200-native (sm_100a) GeoT segment-reduction library
+ * (libgeot.so, built from paper_2404_03019_b200/csrc/).
+ *
+ * Operation (§II-B "Segment Reduction"): given a sorted
+ * (non-decreasing) index Idx of length M = |E| and a row-major M x N matrix X
+ * (N = F), produce Y (|V| x N) with
+ *
+ *      Y[s, :] = f over { X[e, :] : Idx[e] == s },   f in {sum, mean, max}
+ *
+ * (f varies per PAPER.md:76, Fig. 2(c); "mainly an engineering effort",
+ * P:523-524).  The fused form (§IV, Listing 3,
+ * `index_segment_reduce(edge_index[0], edge_index[1], x)`) reads
+ * X[e, :] := x[src_idx[e], :] without materialising X; the weighted fused form
+ * (`index_weight_segment_reduce`, SpMM on sorted COO) reads
+ * X[e, :] := w[e] * x[src_idx[e], :].
+ *
+ * Conventions shared by every entry point:
+ *  - Pointers named d_* / src / idx / x / out / workspace are DEVICE memory
+ *    owned by the caller; the library never allocates, frees or retains them.
+ *    Host pointers are named h_* / cfg.
+ *  - Layout: every matrix is dense row-major with row stride F elements;
+ *    `out` must not alias any input.
+ *  - Values: GEOT_F32 (float) or GEOT_BF16 (bfloat16) inputs; accumulation is
+ *    fp32; `out` has the input dtype (bf16: one round-to-nearest-even of the
+ *    fp32 result).  Indices: GEOT_I32 or GEOT_I64 (all index arrays of one
+ *    call share the type).
+ *  - `out` is WRITE-ONLY: after a successful call every row [0, num_segments)
+ *    is defined, empty segments included (0 for sum, mean and max — reading R1
+ *    of DESIGN.md), so no pre-initialisation is needed.
+ *  - Every call is asynchronous and stream-ordered on `stream`; none performs
+ *    a hidden device->host synchronisation (the segment count is an argument,
+ *    never read from Idx[M-1] as the paper's Python API implies).
+ *  - Synchronous errors are returned immediately: a null pointer where data is
+ *    needed, nnz < 0, num_segments < 0, F < 1, unknown enum, unsupported
+ *    combination, workspace too small, or a CUDA launch error (GEOT_ERR_CUDA).
+ *  - Data-dependent preconditions (Idx sorted, Idx in [seg_base,
+ *    seg_base+num_segments), src_idx in [0, num_x_rows)) are NOT checked on the
+ *    hot path (the paper's precondition "guaranteed by GNN frameworks",
+ *    P:328); geot_validate_index() checks them.  On violating data the kernels
+ *    stay memory-safe (out-of-range rows are skipped, nothing outside `out` is
+ *    written) but the result is unspecified.
+ *  - Determinism: for a fixed configuration the result is bitwise
+ *    reproducible (tile-ordered carry combination, no floating-point atomics).
+ *  - Thread safety: all entry points are re-entrant; the only global state is
+ *    a lazily initialised per-device property cache and a launch counter.
+ */
+#ifndef GEOT_H
+#define GEOT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include <cuda_runtime_api.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GEOT_ABI_VERSION 1
+
+typedef enum {
+    GEOT_OK = 0,
+    GEOT_ERR_INVALID_VALUE = 1,      /* bad scalar argument or null pointer      */
+    GEOT_ERR_UNSUPPORTED = 2,        /* valid but unsupported combination        */
+    GEOT_ERR_WORKSPACE_TOO_SMALL = 3,/* ws_bytes < geot_workspace_size(...)      */
+    GEOT_ERR_UNSORTED_INDEX = 4,     /* reported by geot_validate_index only     */
+    GEOT_ERR_INDEX_OUT_OF_RANGE = 5, /* reported by geot_validate_index only     */
+    GEOT_ERR_SRC_OUT_OF_RANGE = 6,   /* reported by geot_validate_index only     */
+    GEOT_ERR_CUDA = 7                /* a CUDA runtime error (launch, attribute) */
+} geot_status;
+
+typedef enum { GEOT_SUM = 0, GEOT_MEAN = 1, GEOT_MAX = 2 } geot_reduce;
+typedef enum { GEOT_F32 = 0, GEOT_BF16 = 1 } geot_dtype;
+typedef enum { GEOT_I32 = 0, GEOT_I64 = 1 } geot_itype;
+
+/* Kernel variants (the B200 analog of the paper's SR / PR schedules, §III-B,
+ * P:174-216). */
+typedef enum {
+    GEOT_VARIANT_AUTO = 0,      /* let geot_select_config() decide            */
+    GEOT_VARIANT_EDGE_TILE = 1, /* edge-parallel tiles, lane-group sequential
+                                   reduction (SR analog) + in-CTA segmented
+                                   combine + deterministic tile carries        */
+    GEOT_VARIANT_NARROW = 2     /* small F: thread-sequential items + warp
+                                   segmented scan via __shfl_sync (PR/Alg. 1
+                                   analog)                                     */
+} geot_variant;
+
+/* Kernel configuration: the B200 analog of the paper's tunable tuple
+ * <T_N, T_M, M_t, N_t, G_t> (Table I).  Zero fields mean "auto". */
+typedef struct geot_config {
+    int32_t variant;        /* geot_variant                                    */
+    int32_t vec_elems;      /* elements per vector load (VW): f32 {4,1}, bf16 {8,1}  */
+    int32_t lanes_per_row;  /* lanes of one row group (LPR): 1..32, power of 2 */
+    int32_t vecs_per_lane;  /* vectors per lane per row (VPL): 1,2,4,8         */
+    int32_t rows_per_group; /* sequential rows per lane group (R, M_t analog)  */
+    int32_t warps_per_cta;  /* 8 (fixed in ABI v1)                             */
+    int32_t ctas_per_sm;    /* persistent-grid multiplier; 0 = occupancy max   */
+    int32_t reserved;       /* must be 0                                       */
+} geot_config;
+
+/* Human-readable status text (static storage). */
+const char* geot_status_string(geot_status s);
+
+/* ABI version of the loaded library (== GEOT_ABI_VERSION). */
+int geot_abi_version(void);
+
+/* Number of kernels this process has launched through the library (all
+ * devices, all threads) — used by bench.py to report gpu_launches. */
+uint64_t geot_launch_count(void);
+
+/* Measurement hook (bench.py roofline): the NEXT reduction call made by the
+ * calling thread records `before` on its stream immediately before launching
+ * its main reduction kernel and `after` immediately after it, so the caller
+ * can time that kernel alone with CUDA events on the launching stream.
+ * Either may be NULL to clear.  The pair is consumed by that one call. */
+void geot_profile_events(cudaEvent_t before, cudaEvent_t after);
+
+/* H2 kernel selection (P:301-315 data-aware config rules; the generated
+ * decision tree of Listing 5, refit on B200 — DESIGN.md §5).
+ * Pure host code: reads no device memory and launches nothing.
+ * Features: nnz (Idx_size), num_segments (|V|; avg = nnz/num_segments),
+ * F, op, dtype, itype, fused (0/1: index_segment_reduce form).
+ * Writes a complete configuration to *cfg_out. */
+geot_status geot_select_config(int64_t nnz, int64_t num_segments, int64_t F, geot_reduce op,
+                               geot_dtype dtype, geot_itype itype, int fused, geot_config* cfg_out);
+
+/* Workspace (device bytes) the reduction needs for the given problem under
+ * configuration *cfg (NULL = the configuration geot_select_config picks).
+ * The workspace holds per-tile carries; it needs no initialisation and may be
+ * reused by any later call on the same stream. */
+size_t geot_workspace_size(int64_t nnz, int64_t num_segments, int64_t F, geot_reduce op,
+                           geot_dtype dtype, geot_itype itype, int fused, const geot_config* cfg);
+
+/* H4-H7: sorted-index segment reduction (Fig. 2; Alg. 1's result).
+ *   src        [nnz, F] values (dtype), device
+ *   idx        [nnz] non-decreasing segment ids (itype), device
+ *   out        [num_segments, F] (dtype), device, write-only
+ *   workspace  >= geot_workspace_size(..., fused=0, NULL) bytes, device (may be
+ *              NULL when that size is 0)
+ * Returns GEOT_OK or a synchronous error (see conventions). */
+geot_status geot_segment_reduce(const void* src, const void* idx, int64_t nnz, int64_t num_segments,
+                                int64_t F, geot_reduce op, geot_dtype dtype, geot_itype itype, void* out,
+                                void* workspace, size_t ws_bytes, cudaStream_t stream);
+
+/* Extended form used by the multi-GPU shard driver (H9) and by selector
+ * sweeps: segment ids in idx lie in [seg_base, seg_base + num_segments) and
+ * out row r holds segment seg_base + r; *cfg (nullable) overrides selection. */
+geot_status geot_segment_reduce_ex(const void* src, const void* idx, int64_t nnz, int64_t seg_base,
+                                   int64_t num_segments, int64_t F, geot_reduce op, geot_dtype dtype,
+                                   geot_itype itype, void* out, void* workspace, size_t ws_bytes,
+                                   const geot_config* cfg, cudaStream_t stream);
+
+/* H8: fused gather + segment reduction (P:293 index_segment_reduce):
+ *   Y[s,:] = f over { x[src_idx[e], :] : dst_idx[e] == s }.
+ *   x        [num_x_rows, F] node features (dtype), device
+ *   src_idx  [nnz] arbitrary row ids into x (itype), device
+ *   dst_idx  [nnz] non-decreasing segment ids (itype), device
+ *   out      [num_segments, F], device, write-only. */
+geot_status geot_gather_segment_reduce(const void* x, int64_t num_x_rows, const void* src_idx,
+                                       const void* dst_idx, int64_t nnz, int64_t num_segments, int64_t F,
+                                       geot_reduce op, geot_dtype dtype, geot_itype itype, void* out,
+                                       void* workspace, size_t ws_bytes, cudaStream_t stream);
+
+/* Weighted fused form (P:330 index_weight_segment_reduce; SpMM on sorted COO,
+ * P:469): Y[s,:] = sum { w[e] * x[src_idx[e], :] : dst_idx[e] == s }.
+ *   weight [nnz] fp32, device.  Only GEOT_SUM is supported (else
+ *   GEOT_ERR_UNSUPPORTED), as in the paper. */
+geot_status geot_gather_weight_segment_reduce(const void* x, int64_t num_x_rows, const void* src_idx,
+                                              const void* dst_idx, const float* weight, int64_t nnz,
+                                              int64_t num_segments, int64_t F, geot_dtype dtype,
+                                              geot_itype itype, void* out, void* workspace,
+                                              size_t ws_bytes, cudaStream_t stream);
+
+/* Extended fused form: weight nullable (NULL = unweighted), seg_base, cfg. */
+geot_status geot_gather_segment_reduce_ex(const void* x, int64_t num_x_rows, const void* src_idx,
+                                          const void* dst_idx, const float* weight, int64_t nnz,
+                                          int64_t seg_base, int64_t num_segments, int64_t F, geot_reduce op,
+                                          geot_dtype dtype, geot_itype itype, void* out, void* workspace,
+                                          size_t ws_bytes, const geot_config* cfg, cudaStream_t stream);
+
+/* H3: segment offsets (CSR row pointer) of a sorted index:
+ *   offsets[s] = #{ e : idx[e] < s },  s = 0..num_segments  (int64, device,
+ *   num_segments + 1 entries, write-only).  counts[s] = offsets[s+1]-offsets[s].
+ * Bit-exact.  Not needed by geot_segment_reduce (boundaries are detected
+ * inline, the is_seg test of Alg. 1). */
+geot_status geot_segment_offsets(const void* idx, geot_itype itype, int64_t nnz, int64_t num_segments,
+                                 int64_t* offsets, cudaStream_t stream);
+
+/* Precondition check (P:85 sortedness):
+ * writes to *d_status (device int32) a bit mask: 1 = idx not non-decreasing,
+ * 2 = some idx outside [0, num_segments), 4 = some src_idx outside
+ * [0, num_x_rows) (src_idx nullable).  0 = valid.  Asynchronous; the caller
+ * reads *d_status after synchronising. */
+geot_status geot_validate_index(const void* idx, geot_itype itype, int64_t nnz, int64_t num_segments,
+                                const void* src_idx, int64_t num_x_rows, int32_t* d_status,
+                                cudaStream_t stream);
+
+/* H9: multi-GPU partition of the sorted edge stream at segment boundaries
+ * (north_star; reading R18).  For p = 0..nparts:
+ *   t_p = floor(p * nnz / nparts);  s_0 = 0;  s_nparts = num_segments;
+ *   s_p = (t_p == 0) ? 0 : idx[t_p - 1] + 1;   e_p = #{ e : idx[e] < s_p }.
+ * Part p owns output rows [s_p, s_{p+1}) and edges [e_p, e_{p+1}).
+ *   seg_bounds, edge_bounds: int64 [nparts + 1], device, write-only.
+ * Bit-exact. */
+geot_status geot_partition(const void* idx, geot_itype itype, int64_t nnz, int64_t num_segments,
+                           int nparts, int64_t* seg_bounds, int64_t* edge_bounds, cudaStream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GEOT_H */

@@ -1,0 +1,224 @@
+"""B200-native (sm_100a) GeoT segment reduction — thin Python binding of libgeot.
+
+Every computation runs in the library's CUDA kernels (include/geot.h); this
+module only marshals torch tensors (device memory, streams) into the C ABI.
+There is no CPU or PyTorch fallback: a missing library raises on import.
+
+Low-level functions carry the C names (`geot_segment_reduce`, ...).  The
+paper-style API (Listings 2-3) is
+
+    segment_reduce(idx, msg, reduce="sum")
+    index_segment_reduce(src_idx, dst_idx, x, reduce="sum")
+    index_weight_segment_reduce(src_idx, dst_idx, weight, x)
+
+with an optional `num_segments`; when omitted it is idx[-1] + 1, which reads
+one element back to the host (a synchronisation — pass it to avoid that).
+"""
+from __future__ import annotations
+
+import ctypes
+import threading
+
+import torch
+
+from . import _lib
+from ._lib import GeotConfig, GeotError  # noqa: F401
+
+_L = _lib.load()  # raises if libgeot.so is absent: no fallback
+
+__all__ = [
+    "geot_segment_reduce", "geot_gather_segment_reduce", "geot_gather_weight_segment_reduce",
+    "geot_segment_offsets", "geot_validate_index", "geot_partition", "geot_select_config",
+    "geot_workspace_size", "geot_launch_count", "segment_reduce", "index_segment_reduce",
+    "index_weight_segment_reduce", "GeotConfig", "GeotError",
+]
+
+_OPS = {"sum": _lib.SUM, "mean": _lib.MEAN, "max": _lib.MAX}
+_DT = {torch.float32: _lib.F32, torch.bfloat16: _lib.BF16}
+_IT = {torch.int32: _lib.I32, torch.int64: _lib.I64}
+
+
+def _op(reduce):
+    try:
+        return _OPS[reduce]
+    except KeyError:
+        raise ValueError(f"reduce must be one of {sorted(_OPS)}, got {reduce!r}") from None
+
+
+def _dt(t):
+    try:
+        return _DT[t.dtype]
+    except KeyError:
+        raise TypeError(f"values must be float32 or bfloat16, got {t.dtype}") from None
+
+
+def _it(t):
+    try:
+        return _IT[t.dtype]
+    except KeyError:
+        raise TypeError(f"indices must be int32 or int64, got {t.dtype}") from None
+
+
+def _dev(*ts):
+    for t in ts:
+        if t is not None:
+            if not t.is_cuda:
+                raise ValueError("libgeot operates on CUDA tensors only (no CPU path)")
+            if not t.is_contiguous():
+                raise ValueError("tensors must be contiguous (row-major, row stride F)")
+    return next(t for t in ts if t is not None).device
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(dev):
+    return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+
+
+def _cfgp(cfg):
+    if cfg is None:
+        return None
+    if isinstance(cfg, dict):
+        c = GeotConfig()
+        for k, v in cfg.items():
+            setattr(c, k, int(v))
+        cfg = c
+    return ctypes.byref(cfg)
+
+
+# per-(device, stream) growing workspace; the library needs no initialisation
+_ws_lock = threading.Lock()
+_ws_cache: dict = {}
+
+
+def _workspace(dev, nbytes):
+    if nbytes == 0:
+        return None, 0
+    key = (dev, torch.cuda.current_stream(dev).cuda_stream)
+    with _ws_lock:
+        buf = _ws_cache.get(key)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=dev)
+            _ws_cache[key] = buf
+    return buf, buf.numel()
+
+
+def geot_launch_count() -> int:
+    return int(_L.geot_launch_count())
+
+
+def geot_select_config(nnz, num_segments, F, op="sum", dtype=torch.float32, itype=torch.int32, fused=False):
+    c = GeotConfig()
+    _lib.check(_L.geot_select_config(nnz, num_segments, F, _op(op), _DT[dtype], _IT[itype], int(fused),
+                                     ctypes.byref(c)), "geot_select_config")
+    return c
+
+
+def geot_workspace_size(nnz, num_segments, F, op="sum", dtype=torch.float32, itype=torch.int32, fused=False,
+                        cfg=None) -> int:
+    return int(_L.geot_workspace_size(nnz, num_segments, F, _op(op), _DT[dtype], _IT[itype], int(fused),
+                                      _cfgp(cfg)))
+
+
+def _num_segments(idx, num_segments):
+    if num_segments is not None:
+        return int(num_segments)
+    return int(idx[-1].item()) + 1 if idx.numel() else 0  # device->host read (documented)
+
+
+def geot_segment_reduce(src, idx, num_segments=None, op="sum", out=None, seg_base=0, cfg=None):
+    """out[r,:] = op over {src[e,:] : idx[e] == seg_base + r}."""
+    dev = _dev(src, idx, out)
+    if src.dim() != 2 or idx.dim() != 1 or src.shape[0] != idx.shape[0]:
+        raise ValueError("src must be [nnz, F] and idx [nnz]")
+    S = _num_segments(idx, num_segments) - (seg_base if num_segments is None else 0)
+    E, F = src.shape
+    if out is None:
+        out = torch.empty((S, F), dtype=src.dtype, device=dev)
+    elif out.shape != (S, F) or out.dtype != src.dtype:
+        raise ValueError("out must be [num_segments, F] with src's dtype")
+    ws_n = _L.geot_workspace_size(E, S, F, _op(op), _dt(src), _it(idx), 0, _cfgp(cfg))
+    ws, ws_bytes = _workspace(dev, ws_n)
+    with torch.cuda.device(dev):
+        st = _L.geot_segment_reduce_ex(_ptr(src), _ptr(idx), E, seg_base, S, F, _op(op), _dt(src), _it(idx),
+                                       _ptr(out), _ptr(ws), ws_bytes, _cfgp(cfg), _stream(dev))
+    _lib.check(st, "geot_segment_reduce")
+    return out
+
+
+def geot_gather_segment_reduce(x, src_idx, dst_idx, num_segments=None, op="sum", weight=None, out=None,
+                               seg_base=0, cfg=None):
+    """out[r,:] = op over {w[e] * x[src_idx[e],:] : dst_idx[e] == seg_base + r}."""
+    dev = _dev(x, src_idx, dst_idx, weight, out)
+    if x.dim() != 2 or src_idx.shape != dst_idx.shape or src_idx.dim() != 1:
+        raise ValueError("x must be [V, F]; src_idx and dst_idx [nnz]")
+    if src_idx.dtype != dst_idx.dtype:
+        raise TypeError("src_idx and dst_idx must share one index dtype")
+    if weight is not None and (weight.dtype != torch.float32 or weight.shape != dst_idx.shape):
+        raise ValueError("weight must be float32 [nnz]")
+    S = _num_segments(dst_idx, num_segments) - (seg_base if num_segments is None else 0)
+    V, F = x.shape
+    E = dst_idx.shape[0]
+    if out is None:
+        out = torch.empty((S, F), dtype=x.dtype, device=dev)
+    ws_n = _L.geot_workspace_size(E, S, F, _op(op), _dt(x), _it(dst_idx), 1, _cfgp(cfg))
+    ws, ws_bytes = _workspace(dev, ws_n)
+    with torch.cuda.device(dev):
+        st = _L.geot_gather_segment_reduce_ex(_ptr(x), V, _ptr(src_idx), _ptr(dst_idx), _ptr(weight), E, seg_base,
+                                              S, F, _op(op), _dt(x), _it(dst_idx), _ptr(out), _ptr(ws), ws_bytes,
+                                              _cfgp(cfg), _stream(dev))
+    _lib.check(st, "geot_gather_segment_reduce")
+    return out
+
+
+def geot_gather_weight_segment_reduce(x, src_idx, dst_idx, weight, num_segments=None, out=None):
+    return geot_gather_segment_reduce(x, src_idx, dst_idx, num_segments, "sum", weight=weight, out=out)
+
+
+def geot_segment_offsets(idx, num_segments):
+    """offsets[s] = #{e : idx[e] < s}, s = 0..num_segments (int64, device)."""
+    dev = _dev(idx)
+    off = torch.empty(num_segments + 1, dtype=torch.int64, device=dev)
+    with torch.cuda.device(dev):
+        _lib.check(_L.geot_segment_offsets(_ptr(idx), _it(idx), idx.numel(), num_segments, _ptr(off),
+                                           _stream(dev)), "geot_segment_offsets")
+    return off
+
+
+def geot_validate_index(idx, num_segments, src_idx=None, num_x_rows=0) -> int:
+    """Bit mask (1 unsorted, 2 idx out of range, 4 src out of range); synchronises."""
+    dev = _dev(idx, src_idx)
+    status = torch.empty(1, dtype=torch.int32, device=dev)
+    with torch.cuda.device(dev):
+        _lib.check(_L.geot_validate_index(_ptr(idx), _it(idx), idx.numel(), num_segments, _ptr(src_idx),
+                                          num_x_rows, _ptr(status), _stream(dev)), "geot_validate_index")
+    return int(status.item())
+
+
+def geot_partition(idx, num_segments, nparts):
+    """(seg_bounds, edge_bounds): int64 [nparts+1] device tensors (H9)."""
+    dev = _dev(idx)
+    sb = torch.empty(nparts + 1, dtype=torch.int64, device=dev)
+    eb = torch.empty(nparts + 1, dtype=torch.int64, device=dev)
+    with torch.cuda.device(dev):
+        _lib.check(_L.geot_partition(_ptr(idx), _it(idx), idx.numel(), num_segments, nparts, _ptr(sb), _ptr(eb),
+                                     _stream(dev)), "geot_partition")
+    return sb, eb
+
+
+# ------------------------------------------------------------ paper-style API
+def segment_reduce(idx, msg, reduce="sum", num_segments=None):
+    """geot.segment_reduce(edge_index[1], msg, reduce=...)  — PAPER.md:289."""
+    return geot_segment_reduce(msg, idx, num_segments, reduce)
+
+
+def index_segment_reduce(src_idx, dst_idx, x, reduce="sum", num_segments=None):
+    """geot.index_segment_reduce(edge_index[0], edge_index[1], x, reduce=...) — PAPER.md:293."""
+    return geot_gather_segment_reduce(x, src_idx, dst_idx, num_segments, reduce)
+
+
+def index_weight_segment_reduce(src_idx, dst_idx, weight, x, num_segments=None):
+    """Weighted fused form (SpMM on sorted COO) — PAPER.md:330."""
+    return geot_gather_segment_reduce(x, src_idx, dst_idx, num_segments, "sum", weight=weight)

@@ -1,0 +1,369 @@
+// geot.cu — the C ABI of libgeot (include/geot.h): argument checking, kernel
+// selection hand-off, workspace carving, launches; plus the small integer
+// kernels (offsets H3, validation, partition H9, empty-output fill).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+
+#include "../../include/geot.h"
+#include "launch.cuh"
+#include "select.h"
+
+namespace geot {
+
+std::atomic<unsigned long long> g_launches{0};
+thread_local cudaEvent_t g_prof_before = nullptr, g_prof_after = nullptr;
+
+// ----------------------------------------------------------- device cache
+static int sm_count() {
+    static std::atomic<int> cache[64];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+    int v = cache[dev].load(std::memory_order_relaxed);
+    if (v > 0) return v;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+    cache[dev].store(v, std::memory_order_relaxed);
+    return v;
+}
+
+// ----------------------------------------------------------- small kernels
+// H3: offsets[s] = #{e : idx[e] < s}.  Thread e writes offsets[s] = e for the
+// s in (idx[e-1], idx[e]] (the first edge at or past s); thread E writes E
+// for s in (idx[E-1], S].  Each entry is written exactly once (sorted idx).
+__global__ void offsets_kernel(const void* idx, int idx64, long long E, long long S, long long* offsets) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e <= E; e += stride) {
+        const long long prev = (e == 0) ? -1 : load_index(idx, idx64, e - 1);
+        const long long cur = (e == E) ? S : load_index(idx, idx64, e);
+        long long lo = prev + 1, hi = cur;  // inclusive range of s
+        if (lo < 0) lo = 0;
+        if (hi > S) hi = S;
+        for (long long s = lo; s <= hi; ++s) offsets[s] = e;
+    }
+}
+
+// Precondition check: bit 1 unsorted, 2 idx out of [0,S), 4 src out of [0,V).
+__global__ void validate_kernel(const void* idx, int idx64, long long E, long long S, const void* src,
+                                long long V, int* status) {
+    int bad = 0;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < E; e += stride) {
+        const long long k = load_index(idx, idx64, e);
+        if (k < 0 || k >= S) bad |= 2;
+        if (e > 0 && load_index(idx, idx64, e - 1) > k) bad |= 1;
+        if (src) {
+            const long long r = load_index(src, idx64, e);
+            if (r < 0 || r >= V) bad |= 4;
+        }
+    }
+    bad = __reduce_or_sync(0xffffffffu, bad);
+    if ((threadIdx.x & 31) == 0 && bad) atomicOr(status, bad);
+}
+
+// H9: one thread per bound p in [0, P].
+__global__ void partition_kernel(const void* idx, int idx64, long long E, long long S, int P, long long* seg_b,
+                                 long long* edge_b) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p > P) return;
+    long long sp;
+    if (p == 0)
+        sp = 0;
+    else if (p == P)
+        sp = S;
+    else {
+        const long long tp = (long long)(((unsigned __int128)p * (unsigned __int128)E) / (unsigned __int128)P);
+        sp = (tp == 0) ? 0 : load_index(idx, idx64, tp - 1) + 1;
+    }
+    // e_p = lower_bound(idx, sp)
+    long long lo = 0, hi = E;
+    while (lo < hi) {
+        const long long mid = lo + ((hi - lo) >> 1);
+        if (load_index(idx, idx64, mid) < sp)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    seg_b[p] = sp;
+    edge_b[p] = lo;
+}
+
+// E == 0: every output row is an empty segment -> zero bytes.
+__global__ void zero_fill_kernel(unsigned char* out, long long bytes) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    const long long n16 = ((reinterpret_cast<uintptr_t>(out) & 15) == 0) ? bytes / 16 : 0;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += stride)
+        reinterpret_cast<uint4*>(out)[i] = make_uint4(0, 0, 0, 0);
+    for (long long i = n16 * 16 + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < bytes; i += stride) out[i] = 0;
+}
+
+// ------------------------------------------------------------ workspace
+struct WsLayout {
+    size_t meta = 0, carry_h = 0, carry_t = 0, total = 0;
+};
+static WsLayout ws_layout(long long ntiles, long long F) {
+    WsLayout w;
+    if (ntiles <= 1) return w;  // a single tile never carries
+    w.meta = 0;
+    w.carry_h = align_up((size_t)ntiles * sizeof(TileMeta), 256);
+    w.carry_t = w.carry_h + align_up((size_t)ntiles * (size_t)F * sizeof(float), 256);
+    w.total = w.carry_t + align_up((size_t)ntiles * (size_t)F * sizeof(float), 256);
+    return w;
+}
+
+static long long tile_rows_of(const geot_config& c) { return (long long)(256 / c.lanes_per_row) * c.rows_per_group; }
+
+static long long ntiles_of(long long nnz, const geot_config& c) {
+    const long long tr = tile_rows_of(c);
+    return (nnz + tr - 1) / tr;
+}
+
+static bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+static geot_status from_cuda(cudaError_t e) { return e == cudaSuccess ? GEOT_OK : GEOT_ERR_CUDA; }
+
+// Complete / check a (possibly partial) configuration for a call.
+static geot_status resolve_config(long long nnz, long long S, long long F, geot_reduce op, geot_dtype dt,
+                                  geot_itype it, int fused, const geot_config* user, geot_config* out) {
+    geot_config c;
+    geot_status st = select_config_impl(nnz, S, F, op, dt, it, fused, &c);
+    if (st != GEOT_OK) return st;
+    if (user) {
+        if (user->reserved != 0) return GEOT_ERR_INVALID_VALUE;
+        if (user->variant && user->variant != GEOT_VARIANT_EDGE_TILE) return GEOT_ERR_UNSUPPORTED;
+        if (user->vec_elems) c.vec_elems = user->vec_elems;
+        if (user->lanes_per_row) c.lanes_per_row = user->lanes_per_row;
+        if (user->vecs_per_lane) c.vecs_per_lane = user->vecs_per_lane;
+        if (user->rows_per_group) c.rows_per_group = user->rows_per_group;
+        if (user->warps_per_cta && user->warps_per_cta != 8) return GEOT_ERR_UNSUPPORTED;
+        c.ctas_per_sm = user->ctas_per_sm;
+        const int wide = dt == GEOT_F32 ? 4 : 8;
+        if (c.vec_elems != 1 && c.vec_elems != wide) return GEOT_ERR_UNSUPPORTED;
+        if (F % c.vec_elems) return GEOT_ERR_UNSUPPORTED;
+        const int l = c.lanes_per_row;
+        if (l < 1 || l > 32 || (l & (l - 1))) return GEOT_ERR_UNSUPPORTED;
+        const int v = c.vecs_per_lane;
+        if (!(v == 1 || (l == 32 && (v == 2 || v == 4 || (v == 8 && dt == GEOT_F32))))) return GEOT_ERR_UNSUPPORTED;
+        if (c.rows_per_group < 1 || c.rows_per_group > 1024) return GEOT_ERR_UNSUPPORTED;
+        if (c.ctas_per_sm < 0) return GEOT_ERR_INVALID_VALUE;
+    }
+    *out = c;
+    return GEOT_OK;
+}
+
+static geot_status check_enums(geot_reduce op, geot_dtype dt, geot_itype it) {
+    if ((int)op < 0 || (int)op > 2) return GEOT_ERR_INVALID_VALUE;
+    if ((int)dt < 0 || (int)dt > 1) return GEOT_ERR_INVALID_VALUE;
+    if ((int)it < 0 || (int)it > 1) return GEOT_ERR_INVALID_VALUE;
+    return GEOT_OK;
+}
+
+typedef cudaError_t (*edge_launcher)(const EdgeTileParams&, int, int, int, bool, int, int, cudaStream_t, LaunchInfo*);
+
+static edge_launcher pick_launcher(geot_dtype dt, int mode) {
+    static const edge_launcher table[2][3] = {
+        {launch_edge_tile_f32_plain, launch_edge_tile_f32_gather, launch_edge_tile_f32_gatherw},
+        {launch_edge_tile_bf16_plain, launch_edge_tile_bf16_gather, launch_edge_tile_bf16_gatherw}};
+    return table[dt][mode];
+}
+
+// The shared body of every reduction entry point.
+static geot_status reduce_common(const void* X, long long V, const void* src_idx, const void* idx, const float* w,
+                                 long long nnz, long long seg_base, long long S, long long F, geot_reduce op,
+                                 geot_dtype dt, geot_itype it, void* out, void* ws, size_t ws_bytes,
+                                 const geot_config* user_cfg, cudaStream_t stream, int mode) {
+    geot_status st = check_enums(op, dt, it);
+    if (st != GEOT_OK) return st;
+    if (nnz < 0 || S < 0 || F < 1 || V < 0) return GEOT_ERR_INVALID_VALUE;
+    if (F > (1LL << 30) || nnz > (1LL << 47)) return GEOT_ERR_UNSUPPORTED;
+    if (mode == 2 && op != GEOT_SUM) return GEOT_ERR_UNSUPPORTED;
+    if (S == 0) return GEOT_OK;
+    if (!out) return GEOT_ERR_INVALID_VALUE;
+    if (nnz > 0 && (!X || !idx || (mode >= 1 && !src_idx) || (mode == 2 && !w))) return GEOT_ERR_INVALID_VALUE;
+    const size_t esz = dt == GEOT_F32 ? 4 : 2;
+    if (nnz == 0) {  // every segment is empty
+        const long long bytes = S * F * (long long)esz;
+        const int blocks = (int)std::min<long long>((bytes / 16 + 255) / 256 + 1, (long long)sm_count() * 8);
+        zero_fill_kernel<<<blocks, 256, 0, stream>>>(static_cast<unsigned char*>(out), bytes);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        return from_cuda(cudaGetLastError());
+    }
+    geot_config c;
+    st = resolve_config(nnz, S, F, op, dt, it, mode >= 1, user_cfg, &c);
+    if (st != GEOT_OK) return st;
+    // vector path needs 16-byte aligned row starts of the value/output arrays
+    if (c.vec_elems > 1 && !(aligned(X, 16) && aligned(out, 16))) {
+        if (user_cfg && user_cfg->vec_elems > 1) return GEOT_ERR_UNSUPPORTED;
+        c.vec_elems = 1;
+        select_shape_for_vw(F, dt, &c);
+    }
+    const long long ntiles = ntiles_of(nnz, c);
+    const WsLayout L = ws_layout(ntiles, F);
+    if (L.total > 0) {
+        if (!ws) return GEOT_ERR_INVALID_VALUE;
+        if (ws_bytes < L.total) return GEOT_ERR_WORKSPACE_TOO_SMALL;
+    }
+    EdgeTileParams p{};
+    p.X = X;
+    p.idx = idx;
+    p.src = src_idx;
+    p.w = w;
+    p.out = out;
+    unsigned char* wsb = static_cast<unsigned char*>(ws);
+    p.meta = L.total ? reinterpret_cast<TileMeta*>(wsb + L.meta) : nullptr;
+    p.carry_h = L.total ? reinterpret_cast<float*>(wsb + L.carry_h) : nullptr;
+    p.carry_t = L.total ? reinterpret_cast<float*>(wsb + L.carry_t) : nullptr;
+    p.E = nnz;
+    p.seg_base = seg_base;
+    p.S = S;
+    p.V = V;
+    p.ntiles = ntiles;
+    p.F = (int)F;
+    p.NV = (int)(F / c.vec_elems);
+    p.R = c.rows_per_group;
+    p.tile_rows = (int)tile_rows_of(c);
+    p.op = (int)op;
+    p.idx64 = it == GEOT_I64;
+    edge_launcher fn = pick_launcher(dt, mode);
+    cudaError_t e = fn(p, c.vec_elems, c.lanes_per_row, c.vecs_per_lane, op == GEOT_MAX, c.ctas_per_sm,
+                       sm_count(), stream, nullptr);
+    if (e == cudaErrorNotSupported) return GEOT_ERR_UNSUPPORTED;
+    return from_cuda(e);
+}
+
+}  // namespace geot
+
+using namespace geot;
+
+extern "C" {
+
+const char* geot_status_string(geot_status s) {
+    switch (s) {
+        case GEOT_OK: return "GEOT_OK";
+        case GEOT_ERR_INVALID_VALUE: return "GEOT_ERR_INVALID_VALUE: bad scalar argument or null pointer";
+        case GEOT_ERR_UNSUPPORTED: return "GEOT_ERR_UNSUPPORTED: valid but unsupported combination";
+        case GEOT_ERR_WORKSPACE_TOO_SMALL: return "GEOT_ERR_WORKSPACE_TOO_SMALL";
+        case GEOT_ERR_UNSORTED_INDEX: return "GEOT_ERR_UNSORTED_INDEX";
+        case GEOT_ERR_INDEX_OUT_OF_RANGE: return "GEOT_ERR_INDEX_OUT_OF_RANGE";
+        case GEOT_ERR_SRC_OUT_OF_RANGE: return "GEOT_ERR_SRC_OUT_OF_RANGE";
+        case GEOT_ERR_CUDA: return "GEOT_ERR_CUDA: CUDA runtime error";
+    }
+    return "GEOT_ERR_UNKNOWN";
+}
+
+int geot_abi_version(void) { return GEOT_ABI_VERSION; }
+
+uint64_t geot_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+void geot_profile_events(cudaEvent_t before, cudaEvent_t after) {
+    g_prof_before = before;
+    g_prof_after = after;
+}
+
+geot_status geot_select_config(int64_t nnz, int64_t num_segments, int64_t F, geot_reduce op, geot_dtype dtype,
+                               geot_itype itype, int fused, geot_config* cfg_out) {
+    if (!cfg_out) return GEOT_ERR_INVALID_VALUE;
+    geot_status st = check_enums(op, dtype, itype);
+    if (st != GEOT_OK) return st;
+    if (nnz < 0 || num_segments < 0 || F < 1) return GEOT_ERR_INVALID_VALUE;
+    return select_config_impl(nnz, num_segments, F, op, dtype, itype, fused, cfg_out);
+}
+
+size_t geot_workspace_size(int64_t nnz, int64_t num_segments, int64_t F, geot_reduce op, geot_dtype dtype,
+                           geot_itype itype, int fused, const geot_config* cfg) {
+    if (nnz <= 0 || num_segments <= 0 || F < 1) return 0;
+    if (check_enums(op, dtype, itype) != GEOT_OK) return 0;
+    geot_config c;
+    if (resolve_config(nnz, num_segments, F, op, dtype, itype, fused, cfg, &c) != GEOT_OK) return 0;
+    // the misaligned fallback (VW = 1) never uses more tiles than the chosen shape:
+    // size for the larger of the two so either path fits.
+    geot_config c1 = c;
+    c1.vec_elems = 1;
+    select_shape_for_vw(F, dtype, &c1);
+    const long long nt = std::max(ntiles_of(nnz, c), ntiles_of(nnz, c1));
+    return ws_layout(nt, F).total;
+}
+
+geot_status geot_segment_reduce(const void* src, const void* idx, int64_t nnz, int64_t num_segments, int64_t F,
+                                geot_reduce op, geot_dtype dtype, geot_itype itype, void* out, void* workspace,
+                                size_t ws_bytes, cudaStream_t stream) {
+    return reduce_common(src, nnz, nullptr, idx, nullptr, nnz, 0, num_segments, F, op, dtype, itype, out, workspace,
+                         ws_bytes, nullptr, stream, 0);
+}
+
+geot_status geot_segment_reduce_ex(const void* src, const void* idx, int64_t nnz, int64_t seg_base,
+                                   int64_t num_segments, int64_t F, geot_reduce op, geot_dtype dtype,
+                                   geot_itype itype, void* out, void* workspace, size_t ws_bytes,
+                                   const geot_config* cfg, cudaStream_t stream) {
+    return reduce_common(src, nnz, nullptr, idx, nullptr, nnz, seg_base, num_segments, F, op, dtype, itype, out,
+                         workspace, ws_bytes, cfg, stream, 0);
+}
+
+geot_status geot_gather_segment_reduce(const void* x, int64_t num_x_rows, const void* src_idx, const void* dst_idx,
+                                       int64_t nnz, int64_t num_segments, int64_t F, geot_reduce op,
+                                       geot_dtype dtype, geot_itype itype, void* out, void* workspace,
+                                       size_t ws_bytes, cudaStream_t stream) {
+    return reduce_common(x, num_x_rows, src_idx, dst_idx, nullptr, nnz, 0, num_segments, F, op, dtype, itype, out,
+                         workspace, ws_bytes, nullptr, stream, 1);
+}
+
+geot_status geot_gather_weight_segment_reduce(const void* x, int64_t num_x_rows, const void* src_idx,
+                                              const void* dst_idx, const float* weight, int64_t nnz,
+                                              int64_t num_segments, int64_t F, geot_dtype dtype, geot_itype itype,
+                                              void* out, void* workspace, size_t ws_bytes, cudaStream_t stream) {
+    return reduce_common(x, num_x_rows, src_idx, dst_idx, weight, nnz, 0, num_segments, F, GEOT_SUM, dtype, itype,
+                         out, workspace, ws_bytes, nullptr, stream, 2);
+}
+
+geot_status geot_gather_segment_reduce_ex(const void* x, int64_t num_x_rows, const void* src_idx,
+                                          const void* dst_idx, const float* weight, int64_t nnz, int64_t seg_base,
+                                          int64_t num_segments, int64_t F, geot_reduce op, geot_dtype dtype,
+                                          geot_itype itype, void* out, void* workspace, size_t ws_bytes,
+                                          const geot_config* cfg, cudaStream_t stream) {
+    return reduce_common(x, num_x_rows, src_idx, dst_idx, weight, nnz, seg_base, num_segments, F, op, dtype, itype,
+                         out, workspace, ws_bytes, cfg, stream, weight ? 2 : 1);
+}
+
+geot_status geot_segment_offsets(const void* idx, geot_itype itype, int64_t nnz, int64_t num_segments,
+                                 int64_t* offsets, cudaStream_t stream) {
+    if ((int)itype < 0 || (int)itype > 1) return GEOT_ERR_INVALID_VALUE;
+    if (nnz < 0 || num_segments < 0 || !offsets || (nnz > 0 && !idx)) return GEOT_ERR_INVALID_VALUE;
+    const long long work = nnz + 1;
+    const int blocks = (int)std::min<long long>((work + 255) / 256, (long long)sm_count() * 16);
+    offsets_kernel<<<blocks, 256, 0, stream>>>(idx, itype == GEOT_I64, nnz, num_segments,
+                                               reinterpret_cast<long long*>(offsets));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return from_cuda(cudaGetLastError());
+}
+
+geot_status geot_validate_index(const void* idx, geot_itype itype, int64_t nnz, int64_t num_segments,
+                                const void* src_idx, int64_t num_x_rows, int32_t* d_status, cudaStream_t stream) {
+    if ((int)itype < 0 || (int)itype > 1) return GEOT_ERR_INVALID_VALUE;
+    if (nnz < 0 || num_segments < 0 || num_x_rows < 0 || !d_status || (nnz > 0 && !idx)) return GEOT_ERR_INVALID_VALUE;
+    cudaError_t e = cudaMemsetAsync(d_status, 0, sizeof(int32_t), stream);
+    if (e != cudaSuccess) return GEOT_ERR_CUDA;
+    if (nnz == 0) return GEOT_OK;
+    const int blocks = (int)std::min<long long>((nnz + 255) / 256, (long long)sm_count() * 16);
+    validate_kernel<<<blocks, 256, 0, stream>>>(idx, itype == GEOT_I64, nnz, num_segments, src_idx, num_x_rows,
+                                                reinterpret_cast<int*>(d_status));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return from_cuda(cudaGetLastError());
+}
+
+geot_status geot_partition(const void* idx, geot_itype itype, int64_t nnz, int64_t num_segments, int nparts,
+                           int64_t* seg_bounds, int64_t* edge_bounds, cudaStream_t stream) {
+    if ((int)itype < 0 || (int)itype > 1) return GEOT_ERR_INVALID_VALUE;
+    if (nnz < 0 || num_segments < 0 || nparts < 1 || nparts > (1 << 20) || !seg_bounds || !edge_bounds ||
+        (nnz > 0 && !idx))
+        return GEOT_ERR_INVALID_VALUE;
+    const int threads = 128;
+    const int blocks = (nparts + 1 + threads - 1) / threads;
+    partition_kernel<<<blocks, threads, 0, stream>>>(idx, itype == GEOT_I64, nnz, num_segments, nparts,
+                                                     reinterpret_cast<long long*>(seg_bounds),
+                                                     reinterpret_cast<long long*>(edge_bounds));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return from_cuda(cudaGetLastError());
+}
+
+}  // extern "C"

@@ -1,0 +1,132 @@
+// launch.cuh — host-side launchers of the kernel family (internal to libgeot).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <mutex>
+#include <unordered_map>
+
+#include "edge_tile.cuh"
+
+namespace geot {
+
+// Incremented once per kernel launch issued by the library (geot_launch_count).
+extern std::atomic<unsigned long long> g_launches;
+// geot_profile_events(): events bracketing the next main reduction kernel.
+extern thread_local cudaEvent_t g_prof_before, g_prof_after;
+
+struct LaunchInfo {
+    int grid_x = 0, grid_y = 0, smem = 0;
+};
+
+// Occupancy (CTAs per SM) of one kernel instantiation at a given dynamic smem
+// size; cached per (kernel, smem) because the query costs microseconds.
+struct OccKey {
+    const void* fn;
+    size_t smem;
+    int dev;
+    bool operator==(const OccKey& o) const { return fn == o.fn && smem == o.smem && dev == o.dev; }
+};
+struct OccKeyHash {
+    size_t operator()(const OccKey& k) const {
+        return std::hash<const void*>()(k.fn) ^ (k.smem * 0x9E3779B97F4A7C15ull) ^ ((size_t)k.dev << 48);
+    }
+};
+
+template <typename K>
+int cached_occupancy(K kernel, int threads, size_t smem) {
+    static std::mutex mu;
+    static std::unordered_map<OccKey, int, OccKeyHash> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const OccKey key{reinterpret_cast<const void*>(kernel), smem, dev};
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    int occ = 0;
+    if (smem > 48 * 1024 &&
+        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem) != cudaSuccess) occ = 0;
+    cache[key] = occ;
+    return occ;
+}
+
+template <typename T, int VW, int LPR, int VPL, int MODE, bool ISMAX>
+cudaError_t run_edge_tile(const EdgeTileParams& p, int ctas_per_sm, int nsm, cudaStream_t st, LaunchInfo* li) {
+    using Sh = TileShape<LPR, VPL, VW>;
+    auto kern = edge_tile_kernel<T, VW, LPR, VPL, MODE, ISMAX>;
+    const size_t smem = edge_tile_smem_bytes<LPR, VPL, VW>(p.tile_rows, MODE);
+    if (smem > 227 * 1024) return cudaErrorInvalidValue;
+    int occ = cached_occupancy(kern, 256, smem);
+    if (occ <= 0) return cudaErrorInvalidConfiguration;
+    if (ctas_per_sm > 0 && ctas_per_sm < occ) occ = ctas_per_sm;
+    long long gx = (long long)nsm * occ;
+    if (gx > p.ntiles) gx = p.ntiles;
+    const int gy = (p.NV + Sh::FTV - 1) / Sh::FTV;
+    dim3 grid((unsigned)gx, (unsigned)gy);
+    if (g_prof_before) cudaEventRecord(g_prof_before, st);
+    kern<<<grid, 256, smem, st>>>(p);
+    if (g_prof_after) cudaEventRecord(g_prof_after, st);
+    g_prof_before = g_prof_after = nullptr;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (li) {
+        li->grid_x = (int)gx;
+        li->grid_y = gy;
+        li->smem = (int)smem;
+    }
+    if (p.ntiles > 1) {
+        const long long fb = (p.ntiles + 7) / 8;
+        carry_fixup_kernel<T, ISMAX><<<(unsigned)fb, 256, 0, st>>>(p);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+    }
+    return cudaSuccess;
+}
+
+// Switch over the compiled (VW, LPR, VPL, ISMAX) set for one (T, MODE).
+// Compiled shapes: LPR in {1,2,4,8,16,32} with VPL = 1, and LPR = 32 with
+// VPL in {2,4,8} (bf16 wide vectors: VPL <= 4).
+template <typename T, int MODE>
+cudaError_t launch_edge_tile(const EdgeTileParams& p, int vw, int lpr, int vpl, bool ismax, int ctas_per_sm,
+                             int nsm, cudaStream_t st, LaunchInfo* li) {
+    constexpr int WIDE = 16 / (int)sizeof(T);
+#define GEOT_SHAPE(VW_, LPR_, VPL_)                                                                  \
+    if (vw == VW_ && lpr == LPR_ && vpl == VPL_) {                                                   \
+        return ismax ? run_edge_tile<T, VW_, LPR_, VPL_, MODE, true>(p, ctas_per_sm, nsm, st, li)    \
+                     : run_edge_tile<T, VW_, LPR_, VPL_, MODE, false>(p, ctas_per_sm, nsm, st, li);  \
+    }
+#define GEOT_SHAPES_FOR_VW(VW_)  \
+    GEOT_SHAPE(VW_, 1, 1)        \
+    GEOT_SHAPE(VW_, 2, 1)        \
+    GEOT_SHAPE(VW_, 4, 1)        \
+    GEOT_SHAPE(VW_, 8, 1)        \
+    GEOT_SHAPE(VW_, 16, 1)       \
+    GEOT_SHAPE(VW_, 32, 1)       \
+    GEOT_SHAPE(VW_, 32, 2)       \
+    GEOT_SHAPE(VW_, 32, 4)
+    GEOT_SHAPES_FOR_VW(WIDE)
+    GEOT_SHAPES_FOR_VW(1)
+    if constexpr (sizeof(T) == 4) {
+        GEOT_SHAPE(WIDE, 32, 8)
+        GEOT_SHAPE(1, 32, 8)
+    }
+#undef GEOT_SHAPES_FOR_VW
+#undef GEOT_SHAPE
+    return cudaErrorNotSupported;
+}
+
+// Explicit instantiation entry points (one translation unit each, compiled in
+// parallel): inst_<dtype>_<mode>.cu
+cudaError_t launch_edge_tile_f32_plain(const EdgeTileParams&, int, int, int, bool, int, int, cudaStream_t, LaunchInfo*);
+cudaError_t launch_edge_tile_f32_gather(const EdgeTileParams&, int, int, int, bool, int, int, cudaStream_t, LaunchInfo*);
+cudaError_t launch_edge_tile_f32_gatherw(const EdgeTileParams&, int, int, int, bool, int, int, cudaStream_t, LaunchInfo*);
+cudaError_t launch_edge_tile_bf16_plain(const EdgeTileParams&, int, int, int, bool, int, int, cudaStream_t, LaunchInfo*);
+cudaError_t launch_edge_tile_bf16_gather(const EdgeTileParams&, int, int, int, bool, int, int, cudaStream_t, LaunchInfo*);
+cudaError_t launch_edge_tile_bf16_gatherw(const EdgeTileParams&, int, int, int, bool, int, int, cudaStream_t, LaunchInfo*);
+
+}  // namespace geot

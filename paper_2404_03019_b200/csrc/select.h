@@ -1,0 +1,16 @@
+// select.h — H2 kernel selection (pure host code).
+#pragma once
+
+#include "../../include/geot.h"
+
+namespace geot {
+
+// Full configuration for a problem (§III-C: O(1) features
+// Idx_size, avg = Idx_size / Idx_max, F -> configuration tuple).
+geot_status select_config_impl(long long nnz, long long S, long long F, geot_reduce op, geot_dtype dt,
+                               geot_itype it, int fused, geot_config* out);
+
+// Derive the lane shape (LPR, VPL) and rows-per-group for c->vec_elems.
+void select_shape_for_vw(long long F, geot_dtype dt, geot_config* c);
+
+}  // namespace geot

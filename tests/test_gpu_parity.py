@@ -1,0 +1,263 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element
+by element, on the same seeded inputs.  Needs a B200 (marker `gpu`)."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from parity_helpers import check, from_torch_vals, make_case, to_torch_vals
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def geot():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2404_03019_b200 as g
+    return g
+
+
+def run_reduce(geot, X, idx, S, op, itype="i32", cfg=None, seg_base=0):
+    it = torch.int32 if itype == "i32" else torch.int64
+    xt = to_torch_vals(X)
+    it_ = torch.from_numpy(idx).to(it).cuda()
+    y = geot.geot_segment_reduce(xt, it_, S, op, cfg=cfg, seg_base=seg_base)
+    torch.cuda.synchronize()
+    return from_torch_vals(y)
+
+
+def parity(geot, E, S, F, op, dtype="f32", mode="real", kind="powerlaw", seed=0, itype="i32", cfg=None):
+    if op == "max" and mode == "real":
+        mode = "signed"
+    L, idx, X = make_case(E, S, F, dtype, mode, kind, seed)
+    ref = oracle.segment_reduce(X, idx, S, op, nthreads=oracle.default_threads())
+    y = run_reduce(geot, X, idx, S, op, itype, cfg)
+    check(y, ref, op, dtype, mode, counts=L, what=f"E={E} S={S} F={F} {op} {dtype} {mode} {kind} {itype} {cfg}")
+
+
+# ---------------------------------------------------------------- worked examples
+@pytest.mark.parametrize("name", ["W1", "W2"])
+@pytest.mark.parametrize("op", ["sum", "mean", "max"])
+def test_worked_examples_gpu(geot, golden, name, op):
+    g = golden["worked_examples"]
+    x = torch.tensor(g["x"], dtype=torch.float32, device="cuda")
+    c = g[name]
+    dst = torch.tensor(c["dst"], dtype=torch.int64, device="cuda")
+    src = torch.tensor(c["src"], dtype=torch.int64, device="cuda")
+    want = np.array(c[op], dtype=np.float32)
+    y = geot.index_segment_reduce(src, dst, x, op, num_segments=c["S"]).cpu().numpy()
+    np.testing.assert_array_equal(y, want)
+    msg = x[src].contiguous()
+    y2 = geot.segment_reduce(dst, msg, op, num_segments=c["S"]).cpu().numpy()
+    np.testing.assert_array_equal(y2, want)
+    off = geot.geot_segment_offsets(dst, c["S"]).cpu().numpy()
+    np.testing.assert_array_equal(off, c["offsets"])
+    for P, b in c.get("partition", {}).items():
+        sb, eb = geot.geot_partition(dst, c["S"], int(P))
+        np.testing.assert_array_equal(sb.cpu().numpy(), b["seg"])
+        np.testing.assert_array_equal(eb.cpu().numpy(), b["edge"])
+
+
+# ---------------------------------------------------------------- paper-shaped configs
+@pytest.mark.parametrize("op", ["sum", "mean", "max"])
+@pytest.mark.parametrize("mode", ["real", "int"])
+def test_cora_shaped(geot, op, mode):
+    w = synth.workload("cora")
+    parity(geot, w["E"], w["S"], w["F"], op, "f32", mode, "powerlaw", w["seed"])
+
+
+@pytest.mark.parametrize("op", ["sum", "mean", "max"])
+def test_arxiv_shaped_full(geot, op):
+    """configs[1] at full size, in the launch configuration bench.py times."""
+    w = synth.workload("arxiv")
+    parity(geot, w["E"], w["S"], w["F"], op, "f32", "real", "powerlaw", w["seed"])
+
+
+def test_arxiv_shaped_int_mode(geot):
+    w = synth.workload("arxiv")
+    parity(geot, w["E"], w["S"], w["F"], "sum", "f32", "int", "powerlaw", w["seed"])
+
+
+# ---------------------------------------------------------------- widths x skews
+WIDTHS = [1, 2, 3, 4, 8, 16, 31, 32, 64, 96, 128, 256, 1024]
+
+
+@pytest.mark.parametrize("F", WIDTHS)
+@pytest.mark.parametrize("kind", ["powerlaw", "uniform", "gaps"])
+def test_widths_sum(geot, F, kind):
+    E = 40_000 if F <= 256 else 6_000
+    parity(geot, E, E // 9 + 3, F, "sum", "f32", "real", kind, seed=F)
+
+
+@pytest.mark.parametrize("F", [1, 4, 32, 128, 1024])
+@pytest.mark.parametrize("op", ["mean", "max"])
+def test_widths_mean_max(geot, F, op):
+    E = 30_000 if F <= 256 else 5_000
+    parity(geot, E, E // 7, F, op, "f32", "real", "powerlaw", seed=F + 1)
+
+
+@pytest.mark.parametrize("kind", synth.STRESS_KINDS)
+@pytest.mark.parametrize("op", ["sum", "max"])
+def test_stress_families(geot, kind, op):
+    parity(geot, 50_000, 3_000, 64, op, "f32", "int", kind, seed=3)
+
+
+@pytest.mark.parametrize("F", [1, 2, 8, 16, 64, 128, 200, 512])
+@pytest.mark.parametrize("op", ["sum", "mean", "max"])
+def test_bf16(geot, F, op):
+    E = 30_000 if F <= 128 else 6_000
+    parity(geot, E, E // 11, F, op, "bf16", "real", "powerlaw", seed=F + 2)
+    parity(geot, E, E // 11, F, op, "bf16", "int", "powerlaw", seed=F + 3)
+
+
+@pytest.mark.parametrize("F", [1, 4, 64])
+def test_int64_index(geot, F):
+    parity(geot, 30_000, 2_000, F, "sum", "f32", "real", "powerlaw", seed=5, itype="i64")
+    parity(geot, 30_000, 2_000, F, "max", "f32", "real", "gaps", seed=6, itype="i64")
+
+
+# ---------------------------------------------------------------- forced configurations
+@pytest.mark.parametrize("R", [1, 2, 3, 5, 16, 64])
+@pytest.mark.parametrize("vw", [0, 1])
+@pytest.mark.parametrize("F", [4, 32, 128])
+def test_forced_configs(geot, R, vw, F):
+    """Small rows-per-group => many tiles, many carries, middle tiles inside hubs."""
+    cfg = {"rows_per_group": R, "vec_elems": vw, "ctas_per_sm": 1}
+    for op in ("sum", "mean", "max"):
+        parity(geot, 20_000, 700, F, op, "f32", "int", "powerlaw15", seed=R, cfg=cfg)
+
+
+def test_one_hub_across_many_tiles(geot):
+    cfg = {"rows_per_group": 1}
+    for op in ("sum", "mean", "max"):
+        parity(geot, 100_000, 5, 32, op, "f32", "int", "single", seed=1, cfg=cfg)
+        parity(geot, 100_000, 5, 32, op, "f32", "real", "single", seed=1)
+
+
+# ---------------------------------------------------------------- edge cases
+def test_empty_and_degenerate(geot):
+    # E = 0: every row zero, for every op
+    for op in ("sum", "mean", "max"):
+        y = geot.geot_segment_reduce(torch.empty((0, 5), device="cuda"), torch.empty(0, dtype=torch.int32,
+                                                                                   device="cuda"), 7, op)
+        assert y.shape == (7, 5) and torch.all(y == 0) and not torch.any(torch.signbit(y))
+    # S = 0
+    y = geot.geot_segment_reduce(torch.empty((0, 5), device="cuda"), torch.empty(0, dtype=torch.int32,
+                                                                               device="cuda"), 0)
+    assert y.shape == (0, 5)
+    # single edge, leading and trailing empties
+    x = torch.tensor([[2.5, -1.0]], device="cuda")
+    y = geot.geot_segment_reduce(x, torch.tensor([3], dtype=torch.int32, device="cuda"), 6, "max").cpu()
+    assert torch.equal(y, torch.tensor([[0, 0], [0, 0], [0, 0], [2.5, -1.0], [0, 0], [0, 0]]))
+
+
+def test_misaligned_pointers_use_scalar_path(geot):
+    L, idx, X = make_case(5_000, 400, 32, "f32", "int", "powerlaw", 9)
+    big = torch.zeros(X.size + 1, dtype=torch.float32, device="cuda")
+    big[1:] = torch.from_numpy(X.ravel()).cuda()
+    xt = big[1:].view(X.shape)  # 4-byte aligned only
+    assert xt.data_ptr() % 16 != 0
+    it = torch.from_numpy(idx).to(torch.int32).cuda()
+    ref = oracle.segment_reduce(X, idx, 400, "sum")
+    y = geot.geot_segment_reduce(xt, it, 400, "sum")
+    check(y.cpu().numpy(), ref, "sum", "f32", "int")
+
+
+def test_determinism(geot):
+    L, idx, X = make_case(200_000, 5_000, 64, "f32", "real", "powerlaw15", 11)
+    xt, it = to_torch_vals(X), torch.from_numpy(idx).to(torch.int32).cuda()
+    ys = [geot.geot_segment_reduce(xt, it, 5_000, "sum") for _ in range(10)]
+    for y in ys[1:]:
+        assert torch.equal(y.view(torch.int32), ys[0].view(torch.int32))
+
+
+# ---------------------------------------------------------------- fused gather (H8)
+@pytest.mark.parametrize("F", [1, 16, 64, 128])
+@pytest.mark.parametrize("op", ["sum", "mean", "max"])
+def test_fused_gather(geot, F, op):
+    V, E, S = 3_000, 60_000, 2_500
+    mode = "signed" if op == "max" else "real"
+    L = synth.segment_lengths(E, S, "powerlaw", 4)
+    dst = synth.lengths_to_index(L, "i64")
+    src = synth.src_index(1004, 0, E, V)
+    x = synth.values(4, 0, V, F, "f32", mode)
+    ref = oracle.gather_segment_reduce(x, src, dst, S, op, nthreads=oracle.default_threads())
+    for it in (torch.int32, torch.int64):
+        y = geot.index_segment_reduce(torch.from_numpy(src).to(it).cuda(), torch.from_numpy(dst).to(it).cuda(),
+                                      torch.from_numpy(x).cuda(), op, num_segments=S)
+        check(y.cpu().numpy(), ref, op, "f32", mode, counts=L, what=f"fused F={F} {op} {it}")
+
+
+@pytest.mark.parametrize("F", [8, 64])
+def test_fused_bf16_and_weighted(geot, F):
+    V, E, S = 2_000, 40_000, 1_500
+    L = synth.segment_lengths(E, S, "powerlaw", 5)
+    dst = synth.lengths_to_index(L, "i64")
+    src = synth.src_index(1005, 0, E, V)
+    xb = synth.values(5, 0, V, F, "bf16", "real")
+    ref = oracle.gather_segment_reduce(xb, src, dst, S, "sum")
+    y = geot.index_segment_reduce(torch.from_numpy(src).cuda(), torch.from_numpy(dst).cuda(), to_torch_vals(xb),
+                                  "sum", num_segments=S)
+    check(from_torch_vals(y), ref, "sum", "bf16", "real")
+    x = synth.values(6, 0, V, F, "f32", "real")
+    w = synth.weights(2006, 0, E)
+    refw = oracle.gather_segment_reduce(x, src, dst, S, "sum", weight=w)
+    yw = geot.index_weight_segment_reduce(torch.from_numpy(src).cuda(), torch.from_numpy(dst).cuda(),
+                                          torch.from_numpy(w).cuda(), torch.from_numpy(x).cuda(), num_segments=S)
+    check(yw.cpu().numpy(), refw, "sum", "f32", "real")
+
+
+# ---------------------------------------------------------------- integer kernels
+def test_offsets_partition_validate(geot):
+    for kind in synth.STRESS_KINDS:
+        L = synth.stress_lengths(kind, 50_000, 4_000, 2)
+        idx = synth.lengths_to_index(L, "i64")
+        for it in (torch.int32, torch.int64):
+            t = torch.from_numpy(idx).to(it).cuda()
+            np.testing.assert_array_equal(geot.geot_segment_offsets(t, 4_000).cpu().numpy(),
+                                          oracle.offsets(idx, 4_000))
+            for P in (1, 2, 3, 4, 8, 13):
+                sb, eb = geot.geot_partition(t, 4_000, P)
+                osb, oeb = oracle.partition(idx, 4_000, P)
+                np.testing.assert_array_equal(sb.cpu().numpy(), osb)
+                np.testing.assert_array_equal(eb.cpu().numpy(), oeb)
+            assert geot.geot_validate_index(t, 4_000) == oracle.validate(idx, 4_000) == 0
+    bad = np.array([0, 3, 2, 9], dtype=np.int64)
+    src = np.array([0, 1, 7, 2], dtype=np.int64)
+    assert geot.geot_validate_index(torch.from_numpy(bad).cuda(), 5, torch.from_numpy(src).cuda(), 5) == \
+        oracle.validate(bad, 5, src, 5) == 7
+
+
+# ---------------------------------------------------------------- shards (H9 + seg_base)
+def test_virtual_shards(geot):
+    """Partition, run every shard as an independent call into its slice of out."""
+    w = synth.workload("arxiv")
+    L = synth.segment_lengths(w["E"], w["S"], "powerlaw", w["seed"])
+    idx = synth.lengths_to_index(L, "i64")
+    X = synth.values(w["seed"], 0, w["E"], 32, "f32", "int")
+    ref = oracle.segment_reduce(X, idx, w["S"], "sum", nthreads=oracle.default_threads())
+    xt, it = to_torch_vals(X), torch.from_numpy(idx).to(torch.int32).cuda()
+    for P in (2, 3, 8):
+        sb, eb = [b.cpu().numpy() for b in geot.geot_partition(it, w["S"], P)]
+        out = torch.empty((w["S"], 32), device="cuda")
+        for p in range(P):
+            geot.geot_segment_reduce(xt[eb[p]:eb[p + 1]], it[eb[p]:eb[p + 1]], int(sb[p + 1] - sb[p]), "sum",
+                                     out=out[sb[p]:sb[p + 1]], seg_base=int(sb[p]))
+        check(out.cpu().numpy(), ref, "sum", "f32", "int", what=f"P={P}")
+
+
+# ---------------------------------------------------------------- generator agreement
+def test_device_generator_matches_host():
+    import synth.device as sd
+    for dt, tdt in (("f32", torch.float32), ("bf16", torch.bfloat16)):
+        for mode in ("real", "signed", "int"):
+            d = sd.values(1000, 24, seed=7, e_begin=123_456, dtype=tdt, mode=mode)
+            h = synth.values(7, 123_456, 1000, 24, dt, mode)
+            np.testing.assert_array_equal(from_torch_vals(d), h)
+    L = synth.segment_lengths(100_000, 7_000, "powerlaw", 3)
+    np.testing.assert_array_equal(sd.index_from_lengths(L, torch.int64).cpu().numpy(), synth.lengths_to_index(L))
+    np.testing.assert_array_equal(sd.src_index(5000, 977, 1234, e_begin=99).cpu().numpy(),
+                                  synth.src_index(1234, 99, 5000, 977))
