@@ -234,6 +234,9 @@ def run_ours(args):
     torch.cuda.synchronize()
     # ---- timed region: exactly K steps
     kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for a, b in kev:  # materialise the underlying cudaEvent_t (torch creates it lazily on first record)
+        a.record(stream)
+        b.record(stream)
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     torch.cuda.synchronize()

@@ -81,9 +81,14 @@ typedef enum {
     GEOT_VARIANT_EDGE_TILE = 1, /* edge-parallel tiles, lane-group sequential
                                    reduction (SR analog) + in-CTA segmented
                                    combine + deterministic tile carries        */
-    GEOT_VARIANT_NARROW = 2     /* small F: thread-sequential items + warp
+    GEOT_VARIANT_NARROW = 2,    /* small F: thread-sequential items + warp
                                    segmented scan via __shfl_sync (PR/Alg. 1
                                    analog)                                     */
+    GEOT_VARIANT_STREAM = 3     /* rows >= 128 B, contiguous: persistent CTAs,
+                                   per-warp TMA bulk-copy rings (cp.async.bulk
+                                   + mbarrier), balanced contiguous edge ranges
+                                   per lane group, agent-ordered carries;
+                                   rows_per_group = rows per ring stage       */
 } geot_variant;
 
 /* Kernel configuration: the B200 analog of the paper's tunable tuple
@@ -101,6 +106,10 @@ typedef struct geot_config {
 
 /* Human-readable status text (static storage). */
 const char* geot_status_string(geot_status s);
+
+/* Text of the CUDA error behind the calling thread's last GEOT_ERR_CUDA
+ * ("" if none).  Static storage. */
+const char* geot_last_cuda_error(void);
 
 /* ABI version of the loaded library (== GEOT_ABI_VERSION). */
 int geot_abi_version(void);

@@ -47,6 +47,7 @@ _cfgp = ctypes.POINTER(GeotConfig)
 SIGNATURES = {
     "geot_status_string": ([_i32], ctypes.c_char_p),
     "geot_abi_version": ([], _i32),
+    "geot_last_cuda_error": ([], ctypes.c_char_p),
     "geot_launch_count": ([], ctypes.c_uint64),
     "geot_profile_events": ([_vp, _vp], None),
     "geot_select_config": ([_i64, _i64, _i64, _i32, _i32, _i32, _i32, _cfgp], _i32),
@@ -85,4 +86,6 @@ def load() -> ctypes.CDLL:
 
 def check(status: int, where: str) -> None:
     if status != 0:
+        if status == 7 and _lib is not None:
+            where = f"{where} ({_lib.geot_last_cuda_error().decode()})"
         raise GeotError(status, where)

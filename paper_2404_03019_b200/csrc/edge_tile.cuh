@@ -34,7 +34,8 @@ struct TileShape {
     static constexpr int NG = kWarps * G;      // lane groups per CTA
     static constexpr int FTV = LPR * VPL;      // vectors per feature tile
     static constexpr int FTE = FTV * VW;       // elements per feature tile
-    static constexpr int U = (VPL * VW >= 32) ? 1 : ((VPL * VW >= 16) ? 2 : 4);  // rows in flight
+    // rows in flight per lane group (loads issued before any is consumed)
+    static constexpr int U = (VPL * VW >= 32) ? 2 : ((VPL * VW >= 16) ? 4 : 8);
 };
 
 __host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -145,6 +146,7 @@ __global__ void __launch_bounds__(256) edge_tile_kernel(const EdgeTileParams p) 
         }
     };
 
+    asm volatile("griddepcontrol.launch_dependents;");  // let the fix-up grid launch early (PDL)
     for (long long tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
         const long long A = tile * p.tile_rows;
         const int n = (int)min((long long)p.tile_rows, p.E - A);
@@ -183,70 +185,83 @@ __global__ void __launch_bounds__(256) edge_tile_kernel(const EdgeTileParams p) 
             float acc[VPL][VW];
             set_ident(acc);
 
-            for (int l0 = la; l0 < lb; l0 += U) {
+            // per-lane column offsets (elements) and validity, loop invariant
+            int coff[VPL];
+            bool cok[VPL];
+#pragma unroll
+            for (int j = 0; j < VPL; ++j) {
+                coff[j] = vec_col(j) * VW;
+                cok[j] = vec_col(j) < p.NV;
+            }
+            // MODE 0: rows are contiguous; the row pointer advances by F per row
+            const T* xbase = X + (MODE == 0 ? (A + la) * (long long)F : 0);
+
+            auto fetch = [&](int l, const T* rowp, Raw (&r)[VPL], float& wt, bool& ok) {
+                ok = true;
+                wt = 1.0f;
+                if constexpr (MODE != 0) {
+                    const long long rr = ssrc[l];
+                    ok = (rr >= 0 && rr < p.V);  // memory safety on bad data
+                    rowp = X + (ok ? rr : 0) * (long long)F;
+                    if constexpr (MODE == 2) wt = sw[l];
+                }
+#pragma unroll
+                for (int j = 0; j < VPL; ++j) {
+                    if (ok && cok[j]) {
+                        const Raw* vp = reinterpret_cast<const Raw*>(rowp + coff[j]);
+                        r[j] = (MODE == 0) ? ld_stream(vp) : ld_cached(vp);
+                    } else {
+                        r[j] = Raw{};
+                    }
+                }
+            };
+            auto consume = [&](int l, const Raw (&r)[VPL], float wt, bool ok) {
+                const long long k = skey[l + 1];
+                if (k != cur) {  // is_seg: segment `cur` ended at row l-1
+                    if (first && head_open) {
+                        slot_store(sH, g, acc);
+                        myflags |= TM_HEAD_OPEN;
+                        headEnd = A + l;
+                    } else {
+                        write_row(cur, acc, l - seg_start);
+                    }
+                    first = false;
+                    gap_fill(cur, k);
+                    cur = k;
+                    seg_start = l;
+                    set_ident(acc);
+                }
+                if (ok) {
+#pragma unroll
+                    for (int j = 0; j < VPL; ++j) {
+                        float f[VW];
+                        Cv::unpack(r[j], f);
+#pragma unroll
+                        for (int q = 0; q < VW; ++q) {
+                            const float x = (MODE == 2) ? wt * f[q] : f[q];
+                            acc[j][q] = fold<ISMAX>(acc[j][q], x);
+                        }
+                    }
+                }
+            };
+
+            int l0 = la;
+            for (; l0 + U <= lb; l0 += U) {  // full groups of U rows: no bounds checks
                 Raw raw[U][VPL];
                 float wt[U];
                 bool ok[U];
+                const T* xl = xbase + (long long)(l0 - la) * F;
 #pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int l = l0 + u;
-                    ok[u] = l < lb;
-                    wt[u] = 1.0f;
-                    const T* rowp = X;
-                    if (ok[u]) {
-                        if constexpr (MODE == 0) {
-                            rowp = X + (A + l) * (long long)F;
-                        } else {
-                            const long long r = ssrc[l];
-                            if (r < 0 || r >= p.V) ok[u] = false;  // memory safety on bad data
-                            rowp = X + r * (long long)F;
-                            if constexpr (MODE == 2) wt[u] = sw[l];
-                        }
-                    }
+                for (int u = 0; u < U; ++u) fetch(l0 + u, xl + u * F, raw[u], wt[u], ok[u]);
 #pragma unroll
-                    for (int j = 0; j < VPL; ++j) {
-                        const int v = vec_col(j);
-                        if (ok[u] && v < p.NV) {
-                            const Raw* vp = reinterpret_cast<const Raw*>(rowp + (long long)v * VW);
-                            raw[u][j] = (MODE == 0) ? ld_stream(vp) : ld_cached(vp);
-                        } else {
-                            raw[u][j] = Raw{};
-                        }
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int l = l0 + u;
-                    if (l < lb) {
-                        const long long k = skey[l + 1];
-                        if (k != cur) {  // is_seg: segment `cur` ended at row l-1
-                            if (first && head_open) {
-                                slot_store(sH, g, acc);
-                                myflags |= TM_HEAD_OPEN;
-                                headEnd = A + l;
-                            } else {
-                                write_row(cur, acc, l - seg_start);
-                            }
-                            first = false;
-                            gap_fill(cur, k);
-                            cur = k;
-                            seg_start = l;
-                            set_ident(acc);
-                        }
-                        if (ok[u]) {
-#pragma unroll
-                            for (int j = 0; j < VPL; ++j) {
-                                float f[VW];
-                                Cv::unpack(raw[u][j], f);
-#pragma unroll
-                                for (int q = 0; q < VW; ++q) {
-                                    const float x = (MODE == 2) ? wt[u] * f[q] : f[q];
-                                    acc[j][q] = fold<ISMAX>(acc[j][q], x);
-                                }
-                            }
-                        }
-                    }
-                }
+                for (int u = 0; u < U; ++u) consume(l0 + u, raw[u], wt[u], ok[u]);
+            }
+            for (; l0 < lb; ++l0) {  // ragged remainder
+                Raw raw[VPL];
+                float wt;
+                bool ok;
+                fetch(l0, xbase + (long long)(l0 - la) * F, raw, wt, ok);
+                consume(l0, raw, wt, ok);
             }
             const bool tail_open = (skey[lb + 1] == cur);
             if (first && head_open) {
@@ -324,6 +339,7 @@ __global__ void __launch_bounds__(256) edge_tile_kernel(const EdgeTileParams p) 
 // head carry, in fp64, and writes the output row once.
 template <typename T, bool ISMAX>
 __global__ void __launch_bounds__(256) carry_fixup_kernel(const EdgeTileParams p) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // the reduction kernel's carries are complete
     const int lane = threadIdx.x & 31;
     const long long t = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (t >= p.ntiles) return;

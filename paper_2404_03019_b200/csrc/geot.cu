@@ -112,6 +112,13 @@ static WsLayout ws_layout(long long ntiles, long long F) {
     return w;
 }
 
+long long stream_agents(long long nnz, int lpr, int vpl, int nsm) {
+    const long long per_cta = (long long)stream_warps(vpl) * (32 / lpr);
+    long long grid = nnz / per_cta;
+    if (grid > nsm) grid = nsm;
+    return grid >= 1 ? grid * per_cta : 0;
+}
+
 static long long tile_rows_of(const geot_config& c) { return (long long)(256 / c.lanes_per_row) * c.rows_per_group; }
 
 static long long ntiles_of(long long nnz, const geot_config& c) {
@@ -121,7 +128,12 @@ static long long ntiles_of(long long nnz, const geot_config& c) {
 
 static bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
 
-static geot_status from_cuda(cudaError_t e) { return e == cudaSuccess ? GEOT_OK : GEOT_ERR_CUDA; }
+static thread_local cudaError_t g_last_cuda_error = cudaSuccess;
+static geot_status from_cuda(cudaError_t e) {
+    if (e == cudaSuccess) return GEOT_OK;
+    g_last_cuda_error = e;
+    return GEOT_ERR_CUDA;
+}
 
 // Complete / check a (possibly partial) configuration for a call.
 static geot_status resolve_config(long long nnz, long long S, long long F, geot_reduce op, geot_dtype dt,
@@ -131,7 +143,28 @@ static geot_status resolve_config(long long nnz, long long S, long long F, geot_
     if (st != GEOT_OK) return st;
     if (user) {
         if (user->reserved != 0) return GEOT_ERR_INVALID_VALUE;
-        if (user->variant && user->variant != GEOT_VARIANT_EDGE_TILE) return GEOT_ERR_UNSUPPORTED;
+        if (user->variant && user->variant != GEOT_VARIANT_EDGE_TILE && user->variant != GEOT_VARIANT_STREAM)
+            return GEOT_ERR_UNSUPPORTED;
+        if (user->variant == GEOT_VARIANT_EDGE_TILE && c.variant != GEOT_VARIANT_EDGE_TILE) {
+            // back to the edge-tile defaults before applying the overrides
+            c.variant = GEOT_VARIANT_EDGE_TILE;
+            select_shape_for_vw(F, dt, &c);
+            c.ctas_per_sm = 0;
+        }
+        if (user->variant == GEOT_VARIANT_STREAM && c.variant != GEOT_VARIANT_STREAM) {
+            if (!stream_eligible(nnz, F, dt, fused, c)) return GEOT_ERR_UNSUPPORTED;
+            c.variant = GEOT_VARIANT_STREAM;
+            c.rows_per_group = stream_rows_per_stage(F, dt, c.lanes_per_row, c.vecs_per_lane);
+        }
+        if (c.variant == GEOT_VARIANT_STREAM) {  // shape fixed by F: nothing else to tune
+            if (user->rows_per_group && user->rows_per_group != c.rows_per_group) return GEOT_ERR_UNSUPPORTED;
+            if ((user->vec_elems && user->vec_elems != c.vec_elems) ||
+                (user->lanes_per_row && user->lanes_per_row != c.lanes_per_row) ||
+                (user->vecs_per_lane && user->vecs_per_lane != c.vecs_per_lane))
+                return GEOT_ERR_UNSUPPORTED;
+            *out = c;
+            return GEOT_OK;
+        }
         if (user->vec_elems) c.vec_elems = user->vec_elems;
         if (user->lanes_per_row) c.lanes_per_row = user->lanes_per_row;
         if (user->vecs_per_lane) c.vecs_per_lane = user->vecs_per_lane;
@@ -194,8 +227,60 @@ static geot_status reduce_common(const void* X, long long V, const void* src_idx
     if (st != GEOT_OK) return st;
     // vector path needs 16-byte aligned row starts of the value/output arrays
     if (c.vec_elems > 1 && !(aligned(X, 16) && aligned(out, 16))) {
-        if (user_cfg && user_cfg->vec_elems > 1) return GEOT_ERR_UNSUPPORTED;
+        if (user_cfg && (user_cfg->vec_elems > 1 || user_cfg->variant == GEOT_VARIANT_STREAM))
+            return GEOT_ERR_UNSUPPORTED;
+        c.variant = GEOT_VARIANT_EDGE_TILE;
         c.vec_elems = 1;
+        c.ctas_per_sm = 0;
+        select_shape_for_vw(F, dt, &c);
+    }
+    unsigned char* wsb = static_cast<unsigned char*>(ws);
+    if (c.variant == GEOT_VARIANT_STREAM) {
+        const int nsm = sm_count();
+        const long long NA = stream_agents(nnz, c.lanes_per_row, c.vecs_per_lane, nsm);
+        if (NA > 0) {
+            const WsLayout L = ws_layout(NA, F);
+            if (L.total > 0) {
+                if (!ws) return GEOT_ERR_INVALID_VALUE;
+                if (ws_bytes < L.total) return GEOT_ERR_WORKSPACE_TOO_SMALL;
+            }
+            StreamParams sp{};
+            sp.X = X;
+            sp.idx = idx;
+            sp.out = out;
+            sp.meta = L.total ? reinterpret_cast<TileMeta*>(wsb + L.meta) : nullptr;
+            sp.carry_h = L.total ? reinterpret_cast<float*>(wsb + L.carry_h) : nullptr;
+            sp.carry_t = L.total ? reinterpret_cast<float*>(wsb + L.carry_t) : nullptr;
+            sp.E = nnz;
+            sp.seg_base = seg_base;
+            sp.S = S;
+            sp.NA = NA;
+            sp.F = (int)F;
+            sp.NV = (int)(F / c.vec_elems);
+            sp.RS = c.rows_per_group;
+            sp.row_bytes = (int)(F * (long long)esz);
+            sp.op = (int)op;
+            sp.idx64 = it == GEOT_I64;
+            EdgeTileParams fx{};
+            fx.out = out;
+            fx.meta = sp.meta;
+            fx.carry_h = sp.carry_h;
+            fx.carry_t = sp.carry_t;
+            fx.E = nnz;
+            fx.seg_base = seg_base;
+            fx.S = S;
+            fx.ntiles = NA;
+            fx.F = (int)F;
+            fx.op = (int)op;
+            cudaError_t e = dt == GEOT_F32
+                                ? launch_stream_f32(sp, fx, c.lanes_per_row, c.vecs_per_lane, op == GEOT_MAX, nsm, stream)
+                                : launch_stream_bf16(sp, fx, c.lanes_per_row, c.vecs_per_lane, op == GEOT_MAX, nsm, stream);
+            if (e == cudaErrorNotSupported) return GEOT_ERR_UNSUPPORTED;
+            return from_cuda(e);
+        }
+        // too few rows for one per agent: edge-tile kernel with its own shape
+        c.variant = GEOT_VARIANT_EDGE_TILE;
+        c.ctas_per_sm = 0;
         select_shape_for_vw(F, dt, &c);
     }
     const long long ntiles = ntiles_of(nnz, c);
@@ -210,7 +295,6 @@ static geot_status reduce_common(const void* X, long long V, const void* src_idx
     p.src = src_idx;
     p.w = w;
     p.out = out;
-    unsigned char* wsb = static_cast<unsigned char*>(ws);
     p.meta = L.total ? reinterpret_cast<TileMeta*>(wsb + L.meta) : nullptr;
     p.carry_h = L.total ? reinterpret_cast<float*>(wsb + L.carry_h) : nullptr;
     p.carry_t = L.total ? reinterpret_cast<float*>(wsb + L.carry_t) : nullptr;
@@ -256,6 +340,10 @@ int geot_abi_version(void) { return GEOT_ABI_VERSION; }
 
 uint64_t geot_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
+const char* geot_last_cuda_error(void) {
+    return g_last_cuda_error == cudaSuccess ? "" : cudaGetErrorString(g_last_cuda_error);
+}
+
 void geot_profile_events(cudaEvent_t before, cudaEvent_t after) {
     g_prof_before = before;
     g_prof_after = after;
@@ -281,7 +369,15 @@ size_t geot_workspace_size(int64_t nnz, int64_t num_segments, int64_t F, geot_re
     geot_config c1 = c;
     c1.vec_elems = 1;
     select_shape_for_vw(F, dtype, &c1);
-    const long long nt = std::max(ntiles_of(nnz, c), ntiles_of(nnz, c1));
+    long long nt = ntiles_of(nnz, c1);
+    if (c.variant == GEOT_VARIANT_STREAM) {
+        geot_config c2 = c;
+        select_shape_for_vw(F, dtype, &c2);  // its edge-tile fallback shape
+        nt = std::max(nt, ntiles_of(nnz, c2));
+        nt = std::max(nt, stream_agents(nnz, c.lanes_per_row, c.vecs_per_lane, sm_count()));
+    } else {
+        nt = std::max(nt, ntiles_of(nnz, c));
+    }
     return ws_layout(nt, F).total;
 }
 

@@ -8,6 +8,7 @@
 #include <unordered_map>
 
 #include "edge_tile.cuh"
+#include "stream.cuh"
 
 namespace geot {
 
@@ -34,23 +35,54 @@ struct OccKeyHash {
     }
 };
 
+// The kernel's max-dynamic-smem attribute is ONE value per (function, device):
+// it is only ever raised (to the largest size seen), never lowered, so a
+// cached smaller size can never leave it below a later launch's need.
 template <typename K>
 int cached_occupancy(K kernel, int threads, size_t smem) {
     static std::mutex mu;
     static std::unordered_map<OccKey, int, OccKeyHash> cache;
+    static std::unordered_map<OccKey, size_t, OccKeyHash> attr_set;  // smem field unused (0)
     int dev = 0;
     cudaGetDevice(&dev);
     const OccKey key{reinterpret_cast<const void*>(kernel), smem, dev};
+    const OccKey fkey{reinterpret_cast<const void*>(kernel), 0, dev};
     std::lock_guard<std::mutex> lk(mu);
+    if (smem > 48 * 1024) {
+        size_t& cur = attr_set[fkey];
+        if (smem > cur) {
+            if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+                return 0;
+            cur = smem;
+        }
+    }
     auto it = cache.find(key);
     if (it != cache.end()) return it->second;
     int occ = 0;
-    if (smem > 48 * 1024 &&
-        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-        return 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem) != cudaSuccess) occ = 0;
     cache[key] = occ;
     return occ;
+}
+
+// H5 fix-up launch: programmatic dependent launch, so its launch overlaps the
+// reduction kernel's tail (the kernel itself waits with griddepcontrol.wait).
+template <typename T, bool ISMAX>
+cudaError_t launch_fixup(const EdgeTileParams& p, cudaStream_t st) {
+    if (p.ntiles <= 1) return cudaSuccess;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)((p.ntiles + 7) / 8));
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, carry_fixup_kernel<T, ISMAX>, p);
+    if (e != cudaSuccess) return e;
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return cudaSuccess;
 }
 
 template <typename T, int VW, int LPR, int VPL, int MODE, bool ISMAX>
@@ -78,15 +110,54 @@ cudaError_t run_edge_tile(const EdgeTileParams& p, int ctas_per_sm, int nsm, cud
         li->grid_y = gy;
         li->smem = (int)smem;
     }
-    if (p.ntiles > 1) {
-        const long long fb = (p.ntiles + 7) / 8;
-        carry_fixup_kernel<T, ISMAX><<<(unsigned)fb, 256, 0, st>>>(p);
-        e = cudaGetLastError();
-        if (e != cudaSuccess) return e;
-        g_launches.fetch_add(1, std::memory_order_relaxed);
-    }
-    return cudaSuccess;
+    return launch_fixup<T, ISMAX>(p, st);
 }
+
+// Stream kernel: one persistent CTA per SM (fewer when nnz is small so every
+// agent owns >= 1 row).  Returns the agent count through *na (carry slots).
+long long stream_agents(long long nnz, int lpr, int vpl, int nsm);
+
+template <typename T, int LPR, int VPL, bool ISMAX>
+cudaError_t run_stream(const StreamParams& p, const EdgeTileParams& fix, int nsm, cudaStream_t st) {
+    constexpr int VW = 16 / (int)sizeof(T);
+    constexpr int G = 32 / LPR;
+    constexpr int kStreamWarps = stream_warps(VPL);
+    auto kern = stream_kernel<T, VW, LPR, VPL, ISMAX>;
+    const size_t smem = stream_smem_bytes(kStreamWarps, G, p.RS, p.row_bytes);
+    if (smem > 227 * 1024) return cudaErrorNotSupported;
+    if (cached_occupancy(kern, kStreamWarps * 32, smem) <= 0) return cudaErrorInvalidConfiguration;
+    const long long grid = p.NA / ((long long)kStreamWarps * G);
+    if (grid < 1 || grid * kStreamWarps * G != p.NA) return cudaErrorInvalidValue;
+    if (g_prof_before) cudaEventRecord(g_prof_before, st);
+    kern<<<(unsigned)grid, kStreamWarps * 32, smem, st>>>(p);
+    if (g_prof_after) cudaEventRecord(g_prof_after, st);
+    g_prof_before = g_prof_after = nullptr;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return launch_fixup<T, ISMAX>(fix, st);
+}
+
+template <typename T>
+cudaError_t launch_stream(const StreamParams& p, const EdgeTileParams& fix, int lpr, int vpl, bool ismax, int nsm,
+                          cudaStream_t st) {
+#define GEOT_SSHAPE(LPR_, VPL_)                                                              \
+    if (lpr == LPR_ && vpl == VPL_)                                                          \
+        return ismax ? run_stream<T, LPR_, VPL_, true>(p, fix, nsm, st)                      \
+                     : run_stream<T, LPR_, VPL_, false>(p, fix, nsm, st);
+    GEOT_SSHAPE(8, 1)
+    GEOT_SSHAPE(16, 1)
+    GEOT_SSHAPE(32, 1)
+    GEOT_SSHAPE(32, 2)
+    GEOT_SSHAPE(32, 4)
+    if constexpr (sizeof(T) == 4) {
+        GEOT_SSHAPE(32, 8)
+    }
+#undef GEOT_SSHAPE
+    return cudaErrorNotSupported;
+}
+cudaError_t launch_stream_f32(const StreamParams&, const EdgeTileParams&, int, int, bool, int, cudaStream_t);
+cudaError_t launch_stream_bf16(const StreamParams&, const EdgeTileParams&, int, int, bool, int, cudaStream_t);
 
 // Switch over the compiled (VW, LPR, VPL, ISMAX) set for one (T, MODE).
 // Compiled shapes: LPR in {1,2,4,8,16,32} with VPL = 1, and LPR = 32 with

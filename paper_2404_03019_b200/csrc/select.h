@@ -13,4 +13,8 @@ geot_status select_config_impl(long long nnz, long long S, long long F, geot_red
 // Derive the lane shape (LPR, VPL) and rows-per-group for c->vec_elems.
 void select_shape_for_vw(long long F, geot_dtype dt, geot_config* c);
 
+// GEOT_VARIANT_STREAM applicability and its rows per ring stage.
+bool stream_eligible(long long nnz, long long F, geot_dtype dt, int fused, const geot_config& c);
+int stream_rows_per_stage(long long F, geot_dtype dt, int lpr, int vpl);
+
 }  // namespace geot

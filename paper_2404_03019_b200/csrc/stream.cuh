@@ -1,0 +1,291 @@
+// stream.cuh — the TMA-streaming segment-reduction kernel (H4-H7) for rows of
+// >= 128 bytes with contiguous, 16-byte aligned storage: the B200 hot path.
+//
+// Decomposition (the paper's tiling space, re-derived for B200):
+//  * one persistent CTA per SM, W warps; each warp holds G = 32/LPR lane
+//    groups ("agents").  Agent a owns the contiguous row range
+//    [a*E/NA, (a+1)*E/NA) — a perfectly balanced split of the edge stream, so
+//    hub segments never unbalance the grid (the reason for edge-parallel
+//    tiling, SURVEY §7 hard part (b)).
+//  * every warp runs its own NSTAGE-deep ring of shared-memory stages; one
+//    elected lane issues 1-D TMA bulk copies (cp.async.bulk, evict-first) of
+//    each group's next RS rows and arms the stage's mbarrier with the byte
+//    count, while the group's lanes fetch the stage's keys with 4/8-byte
+//    cp.async tracked by the same mbarrier.  The warp consumes a stage once
+//    that mbarrier phase completes.  No block-wide barrier on the hot path.
+//  * each agent reduces its rows sequentially in fp32 registers (SR),
+//    detects the segment heads of a whole stage at once with the is_seg test
+//    of Alg. 1 (key != previous key, one ballot), stores each
+//    complete segment once, zero-fills gaps, and hands its head / tail partial
+//    segments to per-agent carries combined in agent order by
+//    carry_fixup_kernel (edge_tile.cuh).
+#pragma once
+
+#include "common.cuh"
+#include "edge_tile.cuh"
+
+namespace geot {
+
+constexpr int kStreamStages = 4;
+// warps per CTA: 16 (more consumers to hide shared-memory latency) unless a
+// lane holds >= 4 vectors per row (register budget of 512 threads).
+__host__ __device__ constexpr int stream_warps(int vpl) { return vpl >= 4 ? 8 : 16; }
+// rows per lane group per stage: stages of <= 3 KB (16 warps) / 6 KB (8 warps),
+// i.e. 4 stages x W warps <= 192 KB of ring per CTA.
+__host__ __device__ constexpr int stream_rs(int vpl) { return vpl == 1 ? 6 : (vpl == 8 ? 1 : 3); }
+
+struct StreamParams {
+    const void* X;
+    const void* idx;
+    void* out;
+    float* carry_h;
+    float* carry_t;
+    TileMeta* meta;
+    long long E, seg_base, S;
+    long long NA;      // agents (= carry slots)
+    int F, NV;         // elements / 16-byte vectors per row
+    int RS;            // rows per group per stage (== stream_rs(VPL))
+    int row_bytes;     // F * sizeof(T)
+    int op;
+    int idx64;
+};
+
+__host__ __device__ inline size_t stream_smem_bytes(int W, int G, int RS, int row_bytes) {
+    return (size_t)W * kStreamStages * G * RS * row_bytes       // row ring
+           + (size_t)W * kStreamStages * G * RS * 8             // key ring
+           + (size_t)W * kStreamStages * 8;                     // mbarriers
+}
+
+template <typename T, int VW, int LPR, int VPL, bool ISMAX>
+__global__ void __launch_bounds__(stream_warps(VPL) * 32, 1) stream_kernel(const StreamParams p) {
+    constexpr int W = stream_warps(VPL);
+    constexpr int RS = stream_rs(VPL);
+    constexpr int G = 32 / LPR;
+    constexpr int NS = kStreamStages;
+    using Cv = Conv<T, VW>;
+    using Raw = typename Cv::Raw;
+    static_assert(sizeof(Raw) == 16, "stream kernel moves 16-byte vectors");
+    static_assert(RS <= LPR, "one key per lane per stage");
+
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int gi = lane / LPR, li = lane % LPR;
+    const unsigned gmask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (gi * LPR));
+    const int row_bytes = p.row_bytes;
+    const int stage_bytes = G * RS * row_bytes;
+    unsigned char* wbuf = smem_raw + (size_t)warp * NS * stage_bytes;
+    unsigned long long* wkey =
+        reinterpret_cast<unsigned long long*>(smem_raw + (size_t)W * NS * stage_bytes) + warp * NS * G * RS;
+    uint64_t* bars =
+        reinterpret_cast<uint64_t*>(smem_raw + (size_t)W * NS * stage_bytes + (size_t)W * NS * G * RS * 8) + warp * NS;
+
+    const long long seg_lo = p.seg_base, seg_hi = p.seg_base + p.S;
+    const int F = p.F;
+    const T* __restrict__ X = static_cast<const T*>(p.X);
+    T* __restrict__ out = static_cast<T*>(p.out);
+    const int isz = p.idx64 ? 8 : 4;
+    const unsigned char* idxb = static_cast<const unsigned char*>(p.idx);
+
+    // agent ranges (one 64-bit division per agent, once)
+    const long long a = ((long long)blockIdx.x * W + warp) * G + gi;
+    const long long e_lo = (a * p.E) / p.NA;
+    const long long e_hi = ((a + 1) * p.E) / p.NA;
+    const int nrows = (int)(e_hi - e_lo);
+    const int nst = (nrows + RS - 1) / RS;
+    const int nst_w = __reduce_max_sync(0xffffffffu, nst);
+    long long glo[G], ghi[G];  // every group's range, for the producer lane
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        glo[g] = __shfl_sync(0xffffffffu, e_lo, g * LPR);
+        ghi[g] = __shfl_sync(0xffffffffu, e_hi, g * LPR);
+    }
+
+    asm volatile("griddepcontrol.launch_dependents;");  // let the fix-up grid launch early (PDL)
+    // int32 keys land in the low half of 8-byte slots: zero the ring once
+    for (int i = lane; i < NS * G * RS; i += 32) wkey[i] = 0ull;
+    if (lane == 0) {
+        for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1 + 32);  // producer + 32 cp.async arrivals
+        fence_mbar_init();
+    }
+    __syncwarp();
+    const uint64_t pol = policy_evict_first();
+
+    // all lanes: fill stage s of every group of the warp into buffer s % NS
+    auto issue = [&](int s) {
+        const int b = s % NS;
+        if (lane == 0) {
+            unsigned char* buf = wbuf + b * stage_bytes;
+            uint32_t total = 0;
+            int cnt[G];
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                long long c = ghi[g] - (glo[g] + (long long)s * RS);
+                c = c < 0 ? 0 : (c > RS ? RS : c);
+                cnt[g] = (int)c;
+                total += (uint32_t)c * row_bytes;
+            }
+            mbar_arrive_expect_tx(&bars[b], total);
+#pragma unroll
+            for (int g = 0; g < G; ++g)
+                if (cnt[g] > 0)
+                    bulk_g2s(buf + g * RS * row_bytes, X + (glo[g] + (long long)s * RS) * F,
+                             (uint32_t)cnt[g] * row_bytes, &bars[b], pol);
+        }
+        const long long e = e_lo + (long long)s * RS + li;
+        if (li < RS && e < e_hi) {
+            void* dst = wkey + (b * G + gi) * RS + li;
+            if (isz == 4)
+                cp_async_4(dst, idxb + e * 4);
+            else
+                cp_async_8(dst, idxb + e * 8);
+        }
+        cp_async_mbar_arrive(&bars[b]);
+    };
+    for (int s = 0; s < NS && s < nst_w; ++s) issue(s);
+
+    const long long prevk = (e_lo > 0) ? load_index(p.idx, p.idx64, e_lo - 1) : KEY_BEFORE;
+    const long long nextk = (e_hi < p.E) ? load_index(p.idx, p.idx64, e_hi) : KEY_AFTER;
+    const long long first_key = (nrows > 0) ? load_index(p.idx, p.idx64, e_lo) : KEY_AFTER;
+
+    auto vec_col = [&](int j) { return li + j * LPR; };
+    auto write_row = [&](long long key, const float (&acc)[VPL][VW], long long count) {
+        if (key < seg_lo || key >= seg_hi) return;
+        T* rowp = out + (key - seg_lo) * (long long)F;
+#pragma unroll
+        for (int j = 0; j < VPL; ++j) {
+            const int v = vec_col(j);
+            if (v < p.NV) {
+                float o[VW];
+#pragma unroll
+                for (int q = 0; q < VW; ++q) o[q] = finalize(acc[j][q], p.op, count);
+                st_vec(reinterpret_cast<Raw*>(rowp + v * VW), Cv::pack(o));
+            }
+        }
+    };
+    auto gap_fill = [&](long long lo_k, long long hi_k) {
+        long long r0 = (lo_k < seg_lo) ? seg_lo : lo_k + 1;
+        long long r1 = (hi_k > seg_hi) ? seg_hi : hi_k;
+        float z[VW];
+#pragma unroll
+        for (int q = 0; q < VW; ++q) z[q] = 0.0f;
+        const Raw zr = Cv::pack(z);
+        for (long long r = r0; r < r1; ++r) {
+            T* rowp = out + (r - seg_lo) * (long long)F;
+#pragma unroll
+            for (int j = 0; j < VPL; ++j) {
+                const int v = vec_col(j);
+                if (v < p.NV) st_vec(reinterpret_cast<Raw*>(rowp + v * VW), zr);
+            }
+        }
+    };
+    auto carry_store = [&](float* carry, const float (&acc)[VPL][VW]) {
+        float* c = carry + a * (long long)F;
+#pragma unroll
+        for (int j = 0; j < VPL; ++j) {
+            const int v = vec_col(j);
+            if (v < p.NV)
+#pragma unroll
+                for (int q = 0; q < VW; ++q) c[v * VW + q] = acc[j][q];
+        }
+    };
+    float acc[VPL][VW];
+#pragma unroll
+    for (int j = 0; j < VPL; ++j)
+#pragma unroll
+        for (int q = 0; q < VW; ++q) acc[j][q] = identity<ISMAX>();
+
+    long long cur = first_key;
+    const bool head_open = nrows > 0 && prevk == cur;
+    if (nrows > 0 && !head_open) gap_fill(prevk, cur);
+    long long seg_start = e_lo;
+    bool first = true;
+    int flags = 0;
+    long long head_end = 0;
+    bool col_ok[VPL];
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) col_ok[j] = vec_col(j) < p.NV;
+    // 32-bit shared address of this lane's first vector in group gi's rows of buffer 0
+    const uint32_t lane_s0 = smem_u32(wbuf) + gi * RS * row_bytes + li * 16;
+
+#pragma unroll 1
+    for (int s = 0; s < nst_w; ++s) {
+        const int b = s % NS;
+        mbar_wait(&bars[b], (uint32_t)((s / NS) & 1));
+        const uint32_t sbase = lane_s0 + b * stage_bytes;
+        const long long* gkey = reinterpret_cast<const long long*>(wkey + (b * G + gi) * RS);
+        const long long r_base = e_lo + (long long)s * RS;
+        int cnt = (int)(e_hi - r_base);
+        cnt = cnt < 0 ? 0 : (cnt > RS ? RS : cnt);
+        // the whole stage's rows into registers at once (RS x VPL x 16 B per lane)
+        Raw rows[RS][VPL];
+#pragma unroll
+        for (int r = 0; r < RS; ++r)
+#pragma unroll
+            for (int j = 0; j < VPL; ++j)
+                rows[r][j] = (r < cnt && col_ok[j]) ? lds_vec<Raw>(sbase + r * row_bytes + j * LPR * 16) : Raw{};
+        // is_seg of the whole stage (Alg. 1): row r starts a segment iff its
+        // key differs from row r-1's (row -1: `cur`)
+        const long long kmine = (li < cnt) ? gkey[li] : KEY_AFTER;
+        const long long kprev = (li == 0) ? cur : ((li <= cnt) ? gkey[li - 1] : KEY_AFTER);
+        const unsigned heads = __ballot_sync(gmask, li < cnt && kmine != kprev) >> (gi * LPR);
+#pragma unroll
+        for (int r = 0; r < RS; ++r) {
+            if (r >= cnt) break;
+            const Raw (&raw)[VPL] = rows[r];
+            if ((heads >> r) & 1u) {  // segment `cur` ended at the previous row
+                const long long k = gkey[r];
+                const long long e = r_base + r;
+                if (first && head_open) {
+                    carry_store(p.carry_h, acc);
+                    flags |= TM_HEAD_OPEN;
+                    head_end = e;
+                } else {
+                    write_row(cur, acc, e - seg_start);
+                }
+                first = false;
+                gap_fill(cur, k);
+                cur = k;
+                seg_start = e;
+#pragma unroll
+                for (int j = 0; j < VPL; ++j)
+#pragma unroll
+                    for (int q = 0; q < VW; ++q) acc[j][q] = identity<ISMAX>();
+            }
+#pragma unroll
+            for (int j = 0; j < VPL; ++j) {
+                float f[VW];
+                Cv::unpack(raw[j], f);
+#pragma unroll
+                for (int q = 0; q < VW; ++q) acc[j][q] = fold<ISMAX>(acc[j][q], f[q]);
+            }
+        }
+        __syncwarp();
+        if (s + NS < nst_w) issue(s + NS);
+    }
+
+    if (nrows > 0) {
+        const bool tail_open = (nextk == cur);
+        long long tail_start = 0;
+        if (first && head_open) {
+            carry_store(p.carry_h, acc);
+            flags |= TM_HEAD_OPEN;
+            head_end = e_hi;
+            if (tail_open) flags |= TM_TAIL_OPEN | TM_MIDDLE;
+        } else if (tail_open) {
+            carry_store(p.carry_t, acc);
+            flags |= TM_TAIL_OPEN;
+            tail_start = seg_start;
+        } else {
+            write_row(cur, acc, e_hi - seg_start);
+        }
+        if (e_hi == p.E) gap_fill(cur, KEY_AFTER);
+        if (li == 0 && p.meta) {
+            p.meta[a].head_key = first_key;
+            p.meta[a].flags = flags;
+            p.meta[a].head_end = head_end;
+            p.meta[a].tail_start = tail_start;
+        }
+    }
+}
+
+}  // namespace geot

@@ -130,6 +130,45 @@ def test_forced_configs(geot, R, vw, F):
         parity(geot, 20_000, 700, F, op, "f32", "int", "powerlaw15", seed=R, cfg=cfg)
 
 
+STREAM = 3  # GEOT_VARIANT_STREAM
+
+
+@pytest.mark.parametrize("F,dtype", [(32, "f32"), (64, "f32"), (96, "f32"), (128, "f32"), (256, "f32"),
+                                     (1024, "f32"), (64, "bf16"), (128, "bf16"), (512, "bf16")])
+@pytest.mark.parametrize("op", ["sum", "mean", "max"])
+def test_stream_variant(geot, F, dtype, op):
+    E = 70_000 if F <= 256 else 66_000
+    for mode in ("real", "int"):
+        parity(geot, E, E // 7, F, op, dtype, mode, "powerlaw15", seed=F, cfg={"variant": STREAM})
+
+
+@pytest.mark.parametrize("kind", synth.STRESS_KINDS)
+@pytest.mark.parametrize("F", [32, 128, 512])
+def test_stream_stress(geot, kind, F):
+    cfg = {"variant": STREAM}
+    for op in ("sum", "mean", "max"):
+        parity(geot, 100_000, 9_000, F, op, "f32", "int", kind, seed=2, cfg=cfg)
+
+
+def test_stream_int64_and_shards(geot):
+    parity(geot, 300_000, 20_000, 64, "sum", "f32", "real", "powerlaw", seed=4, itype="i64", cfg={"variant": STREAM})
+    L, idx, X = make_case(300_000, 20_000, 128, "f32", "int", "powerlaw15", 5)
+    ref = oracle.segment_reduce(X, idx, 20_000, "sum", nthreads=oracle.default_threads())
+    xt, it = to_torch_vals(X), torch.from_numpy(idx).to(torch.int32).cuda()
+    sb, eb = [b.cpu().numpy() for b in geot.geot_partition(it, 20_000, 3)]
+    out = torch.empty((20_000, 128), device="cuda")
+    for p in range(3):
+        geot.geot_segment_reduce(xt[eb[p]:eb[p + 1]], it[eb[p]:eb[p + 1]], int(sb[p + 1] - sb[p]), "sum",
+                                 out=out[sb[p]:sb[p + 1]], seg_base=int(sb[p]), cfg={"variant": STREAM})
+    check(out.cpu().numpy(), ref, "sum", "f32", "int", what="stream shards")
+
+
+def test_stream_is_default_for_arxiv(geot):
+    w = synth.workload("arxiv")
+    c = geot.geot_select_config(w["E"], w["S"], w["F"], "sum")
+    assert c.variant == STREAM
+
+
 def test_one_hub_across_many_tiles(geot):
     cfg = {"rows_per_group": 1}
     for op in ("sum", "mean", "max"):

@@ -1,0 +1,143 @@
+"""Configuration sweep on the GPU -> performance database (JSONL).
+
+The B200 analog of the paper's offline benchmarking (PAPER.md P:301-309,
+Fig. 5: "we explore a comprehensive range of configurations ... and benchmark
+the outcomes offline on GPUs"; key = features + config, value = throughput).
+
+    python tools/sweep.py --out gpurun_out/perfdb.jsonl [--quick] [--grid NAME]
+
+Every record: workload features (E, S, avg, F, dtype, op, fused, dist,
+max_len), the config tuple, median/min kernel time (CUDA events over the
+launching stream, inputs > L2 or L2 flushed), GB/s (algorithmic bytes) and
+e*F/s.  Inputs come from the device generator (synth.device).
+"""
+from __future__ import annotations
+
+import argparse
+import itertools
+import json
+import os
+import statistics
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2404_03019_b200 as geot  # noqa: E402
+import synth  # noqa: E402
+import synth.device as sd  # noqa: E402
+
+L2_BYTES = 126 * 1024 * 1024
+
+
+def time_call(fn, reps, flush=None, min_ms=0.0):
+    st = torch.cuda.current_stream()
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    t_total = 0.0
+    for i in range(reps):
+        if flush is not None:
+            flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        fn()
+        b.record(st)
+        b.synchronize()
+        ts.append(a.elapsed_time(b))
+        t_total += ts[-1]
+        if i >= 4 and t_total > 2000:
+            break
+    return statistics.median(ts), min(ts)
+
+
+def make_inputs(E, S, F, dtype, dist, seed, fused=False, V=None, itype=torch.int32):
+    L = synth.segment_lengths(E, S, dist, seed)
+    idx = sd.index_from_lengths(L, itype)
+    tdt = torch.float32 if dtype == "f32" else torch.bfloat16
+    if fused:
+        x = sd.values(V, F, seed, dtype=tdt)
+        src = sd.src_index(E, V, seed + 1000, itype=itype)
+        return L, idx, x, src
+    X = sd.values(E, F, seed, dtype=tdt)
+    return L, idx, X, None
+
+
+def candidate_configs(F, dtype, quick=False):
+    base = geot.geot_select_config(1 << 20, 1 << 16, F, "sum", torch.float32 if dtype == "f32" else torch.bfloat16)
+    out = []
+    Rs = [4, 8, 16, 32, 64] if not quick else [8, 32]
+    ctas = [0, 1, 2] if not quick else [0]
+    for R, c in itertools.product(Rs, ctas):
+        out.append({"rows_per_group": R, "ctas_per_sm": c})
+    return base, out
+
+
+def run(args):
+    torch.cuda.init()
+    dev = torch.device("cuda", 0)
+    flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev)
+    f = open(args.out, "a")
+    grid = GRIDS[args.grid]
+    for (E, S, F, dtype, dist, op, fused) in grid:
+        seed = 7
+        V = S
+        L, idx, X, src = make_inputs(E, S, F, dtype, dist, seed, fused, V)
+        esz = 4 if dtype == "f32" else 2
+        B = E * F * esz + E * 4 * (2 if fused else 1) + S * F * esz
+        small = B < 4 * L2_BYTES
+        out = torch.empty((S, F), dtype=X.dtype, device=dev)
+        base, cands = candidate_configs(F, dtype, args.quick)
+        maxlen = int(L.max())
+        for cfg in cands:
+            if fused:
+                fn = lambda: geot.geot_gather_segment_reduce(X, src, idx, S, op, out=out, cfg=cfg)  # noqa: E731
+            else:
+                fn = lambda: geot.geot_segment_reduce(X, idx, S, op, out=out, cfg=cfg)  # noqa: E731
+            try:
+                med, mn = time_call(fn, args.reps, flush if small else None)
+            except Exception as e:  # unsupported config
+                print("skip", cfg, e, file=sys.stderr)
+                continue
+            rec = {"E": E, "S": S, "avg": E / S, "F": F, "dtype": dtype, "op": op, "fused": int(fused), "dist": dist,
+                   "max_len": maxlen, "cfg": {**base.as_dict(), **cfg}, "ms_median": med, "ms_min": mn,
+                   "gbs": B / (med * 1e-3) / 1e9, "efs": E * F / (med * 1e-3), "bytes": B, "l2_flushed": small}
+            f.write(json.dumps(rec) + "\n")
+            f.flush()
+            print(f"E={E} S={S} F={F} {dtype} {dist} {op} fused={int(fused)} {cfg} -> {med * 1e3:.1f} us "
+                  f"{rec['gbs']:.0f} GB/s", flush=True)
+        del X, idx, out, src
+        torch.cuda.empty_cache()
+
+
+ARXIV = (1_166_243, 169_343)
+GRIDS = {
+    "arxiv": [(ARXIV[0], ARXIV[1], 128, "f32", "powerlaw", "sum", False)],
+    "main": [
+        (ARXIV[0], ARXIV[1], 128, "f32", "powerlaw", "sum", False),
+        (1 << 24, 1 << 20, 1, "f32", "powerlaw", "sum", False),
+        (1 << 24, 1 << 20, 4, "f32", "powerlaw", "sum", False),
+        (1 << 24, 1 << 20, 16, "f32", "powerlaw", "sum", False),
+        (1 << 24, 1 << 20, 64, "f32", "powerlaw", "sum", False),
+        (1 << 24, 1 << 20, 64, "f32", "uniform", "sum", False),
+        (1 << 24, 1 << 20, 256, "f32", "powerlaw", "sum", False),
+        (1 << 22, 1 << 18, 1024, "f32", "powerlaw", "sum", False),
+        (61_859_140 // 4, 2_449_029 // 4, 128, "bf16", "powerlaw", "sum", False),
+        (10_556, 2_708, 32, "f32", "powerlaw", "sum", False),
+        (114_615_892 // 8, 232_965, 64, "f32", "powerlaw", "sum", True),
+    ],
+}
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "perfdb.jsonl"))
+    ap.add_argument("--grid", default="arxiv", choices=sorted(GRIDS))
+    ap.add_argument("--reps", type=int, default=30)
+    ap.add_argument("--quick", action="store_true")
+    run(ap.parse_args())
