@@ -98,9 +98,11 @@ typedef struct geot_config {
     int32_t vec_elems;      /* elements per vector load (VW): f32 {4,1}, bf16 {8,1}  */
     int32_t lanes_per_row;  /* lanes of one row group (LPR): 1..32, power of 2 */
     int32_t vecs_per_lane;  /* vectors per lane per row (VPL): 1,2,4,8         */
-    int32_t rows_per_group; /* sequential rows per lane group (R, M_t analog)  */
-    int32_t warps_per_cta;  /* 8 (fixed in ABI v1)                             */
+    int32_t rows_per_group; /* sequential rows per lane group (R, M_t analog);
+                               STREAM: rows per lane group per ring stage     */
+    int32_t warps_per_cta;  /* EDGE_TILE: 8; STREAM: 8 or 16                   */
     int32_t ctas_per_sm;    /* persistent-grid multiplier; 0 = occupancy max   */
+    int32_t stages;         /* STREAM: ring stages per warp (4, 6 or 8)        */
     int32_t reserved;       /* must be 0                                       */
 } geot_config;
 
@@ -136,10 +138,17 @@ geot_status geot_select_config(int64_t nnz, int64_t num_segments, int64_t F, geo
 
 /* Workspace (device bytes) the reduction needs for the given problem under
  * configuration *cfg (NULL = the configuration geot_select_config picks).
- * The workspace holds per-tile carries; it needs no initialisation and may be
- * reused by any later call on the same stream. */
+ * The workspace holds per-agent carries plus a few control words: it must be
+ * zero-filled ONCE before its first use (geot_workspace_init or any memset to
+ * 0); every call leaves it ready for the next one, so it may then be reused by
+ * any number of later calls, in stream order (never by two calls executing
+ * concurrently). */
 size_t geot_workspace_size(int64_t nnz, int64_t num_segments, int64_t F, geot_reduce op,
                            geot_dtype dtype, geot_itype itype, int fused, const geot_config* cfg);
+
+/* Zero-fill a fresh workspace of ws_bytes device bytes on `stream`
+ * (cudaMemsetAsync).  Needed once per workspace allocation. */
+geot_status geot_workspace_init(void* workspace, size_t ws_bytes, cudaStream_t stream);
 
 /* H4-H7: sorted-index segment reduction (Fig. 2; Alg. 1's result).
  *   src        [nnz, F] values (dtype), device

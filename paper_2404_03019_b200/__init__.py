@@ -101,6 +101,8 @@ def _workspace(dev, nbytes):
         buf = _ws_cache.get(key)
         if buf is None or buf.numel() < nbytes:
             buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=dev)
+            with torch.cuda.device(dev):  # zero-filled once (geot_workspace_init)
+                _lib.check(_L.geot_workspace_init(_ptr(buf), buf.numel(), _stream(dev)), "geot_workspace_init")
             _ws_cache[key] = buf
     return buf, buf.numel()
 

@@ -28,7 +28,8 @@ class GeotConfig(ctypes.Structure):
     """Mirror of `geot_config` (include/geot.h)."""
     _fields_ = [("variant", ctypes.c_int32), ("vec_elems", ctypes.c_int32), ("lanes_per_row", ctypes.c_int32),
                 ("vecs_per_lane", ctypes.c_int32), ("rows_per_group", ctypes.c_int32),
-                ("warps_per_cta", ctypes.c_int32), ("ctas_per_sm", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("warps_per_cta", ctypes.c_int32), ("ctas_per_sm", ctypes.c_int32), ("stages", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -52,6 +53,7 @@ SIGNATURES = {
     "geot_profile_events": ([_vp, _vp], None),
     "geot_select_config": ([_i64, _i64, _i64, _i32, _i32, _i32, _i32, _cfgp], _i32),
     "geot_workspace_size": ([_i64, _i64, _i64, _i32, _i32, _i32, _i32, _cfgp], _sz),
+    "geot_workspace_init": ([_vp, _sz, _vp], _i32),
     "geot_segment_reduce": ([_vp, _vp, _i64, _i64, _i64, _i32, _i32, _i32, _vp, _vp, _sz, _vp], _i32),
     "geot_segment_reduce_ex": ([_vp, _vp, _i64, _i64, _i64, _i64, _i32, _i32, _i32, _vp, _vp, _sz, _cfgp, _vp],
                                _i32),

@@ -172,6 +172,21 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
         : "memory");
 }
+// ------------------------------------ inter-CTA publication (release/acquire)
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ int ld_volatile_i32(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
+__device__ __forceinline__ long long ld_volatile_i64(const long long* p) {
+    return *reinterpret_cast<const volatile long long*>(p);
+}
+__device__ __forceinline__ float ld_cg_f32(const float* p) { return __ldcg(p); }  // L2, never a stale L1 line
+
 // Ampere-style async copies of 4 / 8 bytes (keys) into shared memory, tracked
 // by an mbarrier: the arrive fires when all of this thread's prior cp.async
 // operations have completed (.noinc: counted in the barrier's init count).

@@ -99,21 +99,30 @@ __global__ void zero_fill_kernel(unsigned char* out, long long bytes) {
 }
 
 // ------------------------------------------------------------ workspace
+// Layout: [StreamCtrl | 256 B][stream flags: one u64 per possible agent][meta]
+// [carry_h][carry_t].  The control words and flags sit at FIXED offsets for
+// every call and variant, so stale bytes of other regions can never be read as
+// a flag; they must be zero before the workspace's first use.
+static int sm_count();
+static size_t ws_flag_bytes() { return align_up((size_t)sm_count() * 16 * 4 * sizeof(unsigned long long), 256); }
 struct WsLayout {
-    size_t meta = 0, carry_h = 0, carry_t = 0, total = 0;
+    size_t ctrl = 0, flags = 0, meta = 0, carry_h = 0, carry_t = 0, total = 0;
 };
 static WsLayout ws_layout(long long ntiles, long long F) {
     WsLayout w;
     if (ntiles <= 1) return w;  // a single tile never carries
-    w.meta = 0;
-    w.carry_h = align_up((size_t)ntiles * sizeof(TileMeta), 256);
+    w.ctrl = 0;
+    w.flags = 256;
+    w.meta = w.flags + ws_flag_bytes();
+    w.carry_h = w.meta + align_up((size_t)ntiles * sizeof(TileMeta), 256);
     w.carry_t = w.carry_h + align_up((size_t)ntiles * (size_t)F * sizeof(float), 256);
     w.total = w.carry_t + align_up((size_t)ntiles * (size_t)F * sizeof(float), 256);
     return w;
 }
 
-long long stream_agents(long long nnz, int lpr, int vpl, int nsm) {
-    const long long per_cta = (long long)stream_warps(vpl) * (32 / lpr);
+long long stream_agents(long long nnz, int lpr, int warps, int nsm) {
+    if (warps != 8 && warps != 16) return 0;
+    const long long per_cta = (long long)warps * (32 / lpr);
     long long grid = nnz / per_cta;
     if (grid > nsm) grid = nsm;
     return grid >= 1 ? grid * per_cta : 0;
@@ -155,9 +164,15 @@ static geot_status resolve_config(long long nnz, long long S, long long F, geot_
             if (!stream_eligible(nnz, F, dt, fused, c)) return GEOT_ERR_UNSUPPORTED;
             c.variant = GEOT_VARIANT_STREAM;
             c.rows_per_group = stream_rows_per_stage(F, dt, c.lanes_per_row, c.vecs_per_lane);
+            c.warps_per_cta = stream_warps(c.vecs_per_lane);
+            c.stages = stream_stages(c.vecs_per_lane);
+            c.ctas_per_sm = 1;
         }
-        if (c.variant == GEOT_VARIANT_STREAM) {  // shape fixed by F: nothing else to tune
-            if (user->rows_per_group && user->rows_per_group != c.rows_per_group) return GEOT_ERR_UNSUPPORTED;
+        if (c.variant == GEOT_VARIANT_STREAM) {  // lane shape fixed by F; pipeline shape tunable
+            if (user->rows_per_group) c.rows_per_group = user->rows_per_group;
+            if (user->warps_per_cta) c.warps_per_cta = user->warps_per_cta;
+            if (user->stages) c.stages = user->stages;
+            // (an uncompiled pipeline shape is refused at launch: GEOT_ERR_UNSUPPORTED)
             if ((user->vec_elems && user->vec_elems != c.vec_elems) ||
                 (user->lanes_per_row && user->lanes_per_row != c.lanes_per_row) ||
                 (user->vecs_per_lane && user->vecs_per_lane != c.vecs_per_lane))
@@ -170,6 +185,7 @@ static geot_status resolve_config(long long nnz, long long S, long long F, geot_
         if (user->vecs_per_lane) c.vecs_per_lane = user->vecs_per_lane;
         if (user->rows_per_group) c.rows_per_group = user->rows_per_group;
         if (user->warps_per_cta && user->warps_per_cta != 8) return GEOT_ERR_UNSUPPORTED;
+        if (user->stages) return GEOT_ERR_UNSUPPORTED;
         c.ctas_per_sm = user->ctas_per_sm;
         const int wide = dt == GEOT_F32 ? 4 : 8;
         if (c.vec_elems != 1 && c.vec_elems != wide) return GEOT_ERR_UNSUPPORTED;
@@ -237,7 +253,7 @@ static geot_status reduce_common(const void* X, long long V, const void* src_idx
     unsigned char* wsb = static_cast<unsigned char*>(ws);
     if (c.variant == GEOT_VARIANT_STREAM) {
         const int nsm = sm_count();
-        const long long NA = stream_agents(nnz, c.lanes_per_row, c.vecs_per_lane, nsm);
+        const long long NA = stream_agents(nnz, c.lanes_per_row, c.warps_per_cta, nsm);
         if (NA > 0) {
             const WsLayout L = ws_layout(NA, F);
             if (L.total > 0) {
@@ -251,6 +267,9 @@ static geot_status reduce_common(const void* X, long long V, const void* src_idx
             sp.meta = L.total ? reinterpret_cast<TileMeta*>(wsb + L.meta) : nullptr;
             sp.carry_h = L.total ? reinterpret_cast<float*>(wsb + L.carry_h) : nullptr;
             sp.carry_t = L.total ? reinterpret_cast<float*>(wsb + L.carry_t) : nullptr;
+            sp.flag = reinterpret_cast<unsigned long long*>(wsb + L.flags);
+            sp.ctrl = reinterpret_cast<StreamCtrl*>(wsb + L.ctrl);
+            if (NA * 8 > (long long)ws_flag_bytes()) return GEOT_ERR_UNSUPPORTED;
             sp.E = nnz;
             sp.seg_base = seg_base;
             sp.S = S;
@@ -273,8 +292,10 @@ static geot_status reduce_common(const void* X, long long V, const void* src_idx
             fx.F = (int)F;
             fx.op = (int)op;
             cudaError_t e = dt == GEOT_F32
-                                ? launch_stream_f32(sp, fx, c.lanes_per_row, c.vecs_per_lane, op == GEOT_MAX, nsm, stream)
-                                : launch_stream_bf16(sp, fx, c.lanes_per_row, c.vecs_per_lane, op == GEOT_MAX, nsm, stream);
+                                ? launch_stream_f32(sp, fx, c.lanes_per_row, c.vecs_per_lane, c.warps_per_cta,
+                                                    c.rows_per_group, c.stages, op == GEOT_MAX, nsm, stream)
+                                : launch_stream_bf16(sp, fx, c.lanes_per_row, c.vecs_per_lane, c.warps_per_cta,
+                                                     c.rows_per_group, c.stages, op == GEOT_MAX, nsm, stream);
             if (e == cudaErrorNotSupported) return GEOT_ERR_UNSUPPORTED;
             return from_cuda(e);
         }
@@ -374,11 +395,17 @@ size_t geot_workspace_size(int64_t nnz, int64_t num_segments, int64_t F, geot_re
         geot_config c2 = c;
         select_shape_for_vw(F, dtype, &c2);  // its edge-tile fallback shape
         nt = std::max(nt, ntiles_of(nnz, c2));
-        nt = std::max(nt, stream_agents(nnz, c.lanes_per_row, c.vecs_per_lane, sm_count()));
+        nt = std::max(nt, stream_agents(nnz, c.lanes_per_row, 16, sm_count()));  // 16 warps: the most agents
     } else {
         nt = std::max(nt, ntiles_of(nnz, c));
     }
     return ws_layout(nt, F).total;
+}
+
+geot_status geot_workspace_init(void* workspace, size_t ws_bytes, cudaStream_t stream) {
+    if (ws_bytes == 0) return GEOT_OK;
+    if (!workspace) return GEOT_ERR_INVALID_VALUE;
+    return from_cuda(cudaMemsetAsync(workspace, 0, ws_bytes, stream));
 }
 
 geot_status geot_segment_reduce(const void* src, const void* idx, int64_t nnz, int64_t num_segments, int64_t F,

@@ -114,50 +114,60 @@ cudaError_t run_edge_tile(const EdgeTileParams& p, int ctas_per_sm, int nsm, cud
 }
 
 // Stream kernel: one persistent CTA per SM (fewer when nnz is small so every
-// agent owns >= 1 row).  Returns the agent count through *na (carry slots).
-long long stream_agents(long long nnz, int lpr, int vpl, int nsm);
+// agent owns >= 1 row).  Agent count = carry slots.
+long long stream_agents(long long nnz, int lpr, int warps, int nsm);
 
-template <typename T, int LPR, int VPL, bool ISMAX>
+template <typename T, int LPR, int VPL, bool ISMAX, int W, int RS, int NS>
 cudaError_t run_stream(const StreamParams& p, const EdgeTileParams& fix, int nsm, cudaStream_t st) {
     constexpr int VW = 16 / (int)sizeof(T);
     constexpr int G = 32 / LPR;
-    constexpr int kStreamWarps = stream_warps(VPL);
-    auto kern = stream_kernel<T, VW, LPR, VPL, ISMAX>;
-    const size_t smem = stream_smem_bytes(kStreamWarps, G, p.RS, p.row_bytes);
+    auto kern = stream_kernel<T, VW, LPR, VPL, ISMAX, W, RS, NS>;
+    const size_t smem = stream_smem_bytes(W, NS, G, RS, p.row_bytes);
     if (smem > 227 * 1024) return cudaErrorNotSupported;
-    if (cached_occupancy(kern, kStreamWarps * 32, smem) <= 0) return cudaErrorInvalidConfiguration;
-    const long long grid = p.NA / ((long long)kStreamWarps * G);
-    if (grid < 1 || grid * kStreamWarps * G != p.NA) return cudaErrorInvalidValue;
+    if (cached_occupancy(kern, W * 32, smem) <= 0) return cudaErrorInvalidConfiguration;
+    const long long grid = p.NA / ((long long)W * G);
+    if (grid < 1 || grid * W * G != p.NA) return cudaErrorInvalidValue;
     if (g_prof_before) cudaEventRecord(g_prof_before, st);
-    kern<<<(unsigned)grid, kStreamWarps * 32, smem, st>>>(p);
+    kern<<<(unsigned)grid, W * 32, smem, st>>>(p);
     if (g_prof_after) cudaEventRecord(g_prof_after, st);
     g_prof_before = g_prof_after = nullptr;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     g_launches.fetch_add(1, std::memory_order_relaxed);
-    return launch_fixup<T, ISMAX>(fix, st);
+    (void)fix;  // carries are resolved inside the stream kernel (no fix-up launch)
+    return cudaSuccess;
 }
 
+// Compiled (lane shape) x (pipeline shape W warps / RS rows per stage / NS
+// stages).  The first pipeline listed for a lane shape is its default.
 template <typename T>
-cudaError_t launch_stream(const StreamParams& p, const EdgeTileParams& fix, int lpr, int vpl, bool ismax, int nsm,
-                          cudaStream_t st) {
-#define GEOT_SSHAPE(LPR_, VPL_)                                                              \
-    if (lpr == LPR_ && vpl == VPL_)                                                          \
-        return ismax ? run_stream<T, LPR_, VPL_, true>(p, fix, nsm, st)                      \
-                     : run_stream<T, LPR_, VPL_, false>(p, fix, nsm, st);
-    GEOT_SSHAPE(8, 1)
-    GEOT_SSHAPE(16, 1)
-    GEOT_SSHAPE(32, 1)
-    GEOT_SSHAPE(32, 2)
-    GEOT_SSHAPE(32, 4)
+cudaError_t launch_stream(const StreamParams& p, const EdgeTileParams& fix, int lpr, int vpl, int w, int rs, int ns,
+                          bool ismax, int nsm, cudaStream_t st) {
+#define GEOT_SSHAPE(LPR_, VPL_, W_, RS_, NS_)                                                         \
+    if (lpr == LPR_ && vpl == VPL_ && w == W_ && rs == RS_ && ns == NS_)                              \
+        return ismax ? run_stream<T, LPR_, VPL_, true, W_, RS_, NS_>(p, fix, nsm, st)                 \
+                     : run_stream<T, LPR_, VPL_, false, W_, RS_, NS_>(p, fix, nsm, st);
+#define GEOT_SSHAPE_V1(LPR_)         \
+    GEOT_SSHAPE(LPR_, 1, 16, 6, 4)   \
+    GEOT_SSHAPE(LPR_, 1, 8, 6, 8)    \
+    GEOT_SSHAPE(LPR_, 1, 16, 3, 8)   \
+    GEOT_SSHAPE(LPR_, 1, 8, 8, 6)
+    GEOT_SSHAPE_V1(8)
+    GEOT_SSHAPE_V1(16)
+    GEOT_SSHAPE_V1(32)
+    GEOT_SSHAPE(32, 2, 16, 3, 4)
+    GEOT_SSHAPE(32, 2, 8, 3, 8)
+    GEOT_SSHAPE(32, 4, 8, 3, 4)
     if constexpr (sizeof(T) == 4) {
-        GEOT_SSHAPE(32, 8)
+        GEOT_SSHAPE(32, 8, 8, 1, 4)
+        GEOT_SSHAPE(32, 8, 8, 1, 6)
     }
+#undef GEOT_SSHAPE_V1
 #undef GEOT_SSHAPE
     return cudaErrorNotSupported;
 }
-cudaError_t launch_stream_f32(const StreamParams&, const EdgeTileParams&, int, int, bool, int, cudaStream_t);
-cudaError_t launch_stream_bf16(const StreamParams&, const EdgeTileParams&, int, int, bool, int, cudaStream_t);
+cudaError_t launch_stream_f32(const StreamParams&, const EdgeTileParams&, int, int, int, int, int, bool, int, cudaStream_t);
+cudaError_t launch_stream_bf16(const StreamParams&, const EdgeTileParams&, int, int, int, int, int, bool, int, cudaStream_t);
 
 // Switch over the compiled (VW, LPR, VPL, ISMAX) set for one (T, MODE).
 // Compiled shapes: LPR in {1,2,4,8,16,32} with VPL = 1, and LPR = 32 with

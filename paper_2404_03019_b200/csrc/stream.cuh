@@ -26,42 +26,50 @@
 
 namespace geot {
 
-constexpr int kStreamStages = 4;
-// warps per CTA: 16 (more consumers to hide shared-memory latency) unless a
-// lane holds >= 4 vectors per row (register budget of 512 threads).
+// Default pipeline shape per lane shape (the selector may pick another compiled
+// one, see launch.cuh): W warps per CTA (16 hides shared-memory latency
+// better; 8 when a lane holds >= 4 vectors per row — register budget), RS rows
+// per lane group per stage, NS stages: NS x W x stage <= ~192 KB of ring.
 __host__ __device__ constexpr int stream_warps(int vpl) { return vpl >= 4 ? 8 : 16; }
-// rows per lane group per stage: stages of <= 3 KB (16 warps) / 6 KB (8 warps),
-// i.e. 4 stages x W warps <= 192 KB of ring per CTA.
 __host__ __device__ constexpr int stream_rs(int vpl) { return vpl == 1 ? 6 : (vpl == 8 ? 1 : 3); }
+__host__ __device__ constexpr int stream_stages(int vpl) { return 4 + 0 * vpl; }
+
+// Control words in the workspace (zero-filled once before first use; the last
+// CTA of every call re-arms ticket/done and advances the epoch, so per-agent
+// flags published in a call (value epoch+1) never need clearing).
+struct StreamCtrl {
+    unsigned ticket;
+    unsigned done;
+    unsigned long long epoch;
+};
 
 struct StreamParams {
     const void* X;
     const void* idx;
     void* out;
-    float* carry_h;
-    float* carry_t;
-    TileMeta* meta;
+    float* carry_h;   // [NA, F] partial of an agent lying wholly inside one segment
+    float* carry_t;   // [NA, F] tail partial of a segment continuing past the agent
+    TileMeta* meta;   // [NA] flags / tail_start of publishing agents
+    unsigned long long* flag;  // [NA] == epoch+1 once the agent's carry is published
+    StreamCtrl* ctrl;
     long long E, seg_base, S;
     long long NA;      // agents (= carry slots)
     int F, NV;         // elements / 16-byte vectors per row
-    int RS;            // rows per group per stage (== stream_rs(VPL))
+    int RS;            // rows per group per stage (== the kernel's RS)
     int row_bytes;     // F * sizeof(T)
     int op;
     int idx64;
 };
 
-__host__ __device__ inline size_t stream_smem_bytes(int W, int G, int RS, int row_bytes) {
-    return (size_t)W * kStreamStages * G * RS * row_bytes       // row ring
-           + (size_t)W * kStreamStages * G * RS * 8             // key ring
-           + (size_t)W * kStreamStages * 8;                     // mbarriers
+__host__ __device__ inline size_t stream_smem_bytes(int W, int NS, int G, int RS, int row_bytes) {
+    return (size_t)W * NS * G * RS * row_bytes       // row ring
+           + (size_t)W * NS * G * RS * 8             // key ring
+           + (size_t)W * NS * 8;                     // mbarriers
 }
 
-template <typename T, int VW, int LPR, int VPL, bool ISMAX>
-__global__ void __launch_bounds__(stream_warps(VPL) * 32, 1) stream_kernel(const StreamParams p) {
-    constexpr int W = stream_warps(VPL);
-    constexpr int RS = stream_rs(VPL);
+template <typename T, int VW, int LPR, int VPL, bool ISMAX, int W, int RS, int NS>
+__global__ void __launch_bounds__(W * 32, 1) stream_kernel(const StreamParams p) {
     constexpr int G = 32 / LPR;
-    constexpr int NS = kStreamStages;
     using Cv = Conv<T, VW>;
     using Raw = typename Cv::Raw;
     static_assert(sizeof(Raw) == 16, "stream kernel moves 16-byte vectors");
@@ -86,8 +94,20 @@ __global__ void __launch_bounds__(stream_warps(VPL) * 32, 1) stream_kernel(const
     const int isz = p.idx64 ? 8 : 4;
     const unsigned char* idxb = static_cast<const unsigned char*>(p.idx);
 
+    // CTA ticket: agents are numbered in CTA start order, so an agent only
+    // ever waits on agents of CTAs that started before it (forward progress).
+    __shared__ unsigned s_ticket;
+    __shared__ unsigned long long s_epoch;
+    if (threadIdx.x == 0) {
+        s_ticket = atomicAdd(&p.ctrl->ticket, 1u);
+        s_epoch = ld_acquire_u64(&p.ctrl->epoch);
+        if (s_ticket >= gridDim.x) __trap();  // workspace not zero-filled before first use
+    }
+    __syncthreads();
+    const unsigned long long pub = s_epoch + 1;  // "published in this call" flag value
+
     // agent ranges (one 64-bit division per agent, once)
-    const long long a = ((long long)blockIdx.x * W + warp) * G + gi;
+    const long long a = ((long long)s_ticket * W + warp) * G + gi;
     const long long e_lo = (a * p.E) / p.NA;
     const long long e_hi = ((a + 1) * p.E) / p.NA;
     const int nrows = (int)(e_hi - e_lo);
@@ -100,7 +120,6 @@ __global__ void __launch_bounds__(stream_warps(VPL) * 32, 1) stream_kernel(const
         ghi[g] = __shfl_sync(0xffffffffu, e_hi, g * LPR);
     }
 
-    asm volatile("griddepcontrol.launch_dependents;");  // let the fix-up grid launch early (PDL)
     // int32 keys land in the low half of 8-byte slots: zero the ring once
     for (int i = lane; i < NS * G * RS; i += 32) wkey[i] = 0ull;
     if (lane == 0) {
@@ -201,6 +220,7 @@ __global__ void __launch_bounds__(stream_warps(VPL) * 32, 1) stream_kernel(const
     bool first = true;
     int flags = 0;
     long long head_end = 0;
+    float hacc[VPL][VW];  // head partial of a segment that began in an earlier agent
     bool col_ok[VPL];
 #pragma unroll
     for (int j = 0; j < VPL; ++j) col_ok[j] = vec_col(j) < p.NV;
@@ -236,7 +256,10 @@ __global__ void __launch_bounds__(stream_warps(VPL) * 32, 1) stream_kernel(const
                 const long long k = gkey[r];
                 const long long e = r_base + r;
                 if (first && head_open) {
-                    carry_store(p.carry_h, acc);
+#pragma unroll
+                    for (int j = 0; j < VPL; ++j)
+#pragma unroll
+                        for (int q = 0; q < VW; ++q) hacc[j][q] = acc[j][q];
                     flags |= TM_HEAD_OPEN;
                     head_end = e;
                 } else {
@@ -263,27 +286,84 @@ __global__ void __launch_bounds__(stream_warps(VPL) * 32, 1) stream_kernel(const
         if (s + NS < nst_w) issue(s + NS);
     }
 
+    // ---- agent end: publish the carries later agents need (H5) ...
     if (nrows > 0) {
         const bool tail_open = (nextk == cur);
-        long long tail_start = 0;
         if (first && head_open) {
-            carry_store(p.carry_h, acc);
             flags |= TM_HEAD_OPEN;
             head_end = e_hi;
-            if (tail_open) flags |= TM_TAIL_OPEN | TM_MIDDLE;
+            if (tail_open) {  // the whole range lies inside one segment
+                flags |= TM_TAIL_OPEN | TM_MIDDLE;
+                carry_store(p.carry_h, acc);
+            } else {
+#pragma unroll
+                for (int j = 0; j < VPL; ++j)
+#pragma unroll
+                    for (int q = 0; q < VW; ++q) hacc[j][q] = acc[j][q];
+            }
         } else if (tail_open) {
             carry_store(p.carry_t, acc);
             flags |= TM_TAIL_OPEN;
-            tail_start = seg_start;
         } else {
             write_row(cur, acc, e_hi - seg_start);
         }
         if (e_hi == p.E) gap_fill(cur, KEY_AFTER);
-        if (li == 0 && p.meta) {
-            p.meta[a].head_key = first_key;
-            p.meta[a].flags = flags;
-            p.meta[a].head_end = head_end;
-            p.meta[a].tail_start = tail_start;
+        if (tail_open) {  // some later agent owns this segment: publish (release)
+            if (li == 0) {
+                p.meta[a].flags = flags;
+                p.meta[a].tail_start = seg_start;
+            }
+            __syncwarp(gmask);
+            __threadfence();
+            if (li == 0) st_release_u64(&p.flag[a], pub);
+        }
+    }
+    __syncwarp();
+    // ---- ... and own the segments that end here but began earlier: combine the
+    // start agent's tail carry, the wholly-covered agents' carries and this
+    // agent's head partial, in agent order (deterministic), write the row once.
+    if (nrows > 0 && (flags & TM_HEAD_OPEN) && !(flags & TM_MIDDLE)) {
+        long long u = a - 1;
+        for (; u >= 0; --u) {  // predecessors are consistent by construction: agent
+                               // u's tail test and agent u+1's head test compare the same keys
+            while (ld_acquire_u64(&p.flag[u]) != pub) {
+            }
+            if (!(ld_volatile_i32(&p.meta[u].flags) & TM_MIDDLE)) break;
+        }
+        if (u < 0) u = 0;  // unreachable (agent 0 never has an open head)
+        const long long count = head_end - ld_volatile_i64(&p.meta[u].tail_start);
+        float tot[VPL][VW];
+#pragma unroll
+        for (int j = 0; j < VPL; ++j) {
+            const int v = vec_col(j);
+#pragma unroll
+            for (int q = 0; q < VW; ++q) tot[j][q] = (v < p.NV) ? ld_cg_f32(p.carry_t + u * (long long)F + v * VW + q) : 0.f;
+        }
+        for (long long m = u + 1; m < a; ++m) {
+#pragma unroll
+            for (int j = 0; j < VPL; ++j) {
+                const int v = vec_col(j);
+#pragma unroll
+                for (int q = 0; q < VW; ++q)
+                    if (v < p.NV) tot[j][q] = fold<ISMAX>(tot[j][q], ld_cg_f32(p.carry_h + m * (long long)F + v * VW + q));
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < VPL; ++j)
+#pragma unroll
+            for (int q = 0; q < VW; ++q) tot[j][q] = fold<ISMAX>(tot[j][q], hacc[j][q]);
+        write_row(first_key, tot, count);
+    }
+    // ---- last CTA out re-arms the control words for the next call
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned done = atomicAdd(&p.ctrl->done, 1u);
+        if (done == gridDim.x - 1) {
+            p.ctrl->done = 0;
+            p.ctrl->ticket = 0;
+            __threadfence();
+            atomicAdd(&p.ctrl->epoch, 1ull);
         }
     }
 }

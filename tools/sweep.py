@@ -68,13 +68,22 @@ def make_inputs(E, S, F, dtype, dist, seed, fused=False, V=None, itype=torch.int
     return L, idx, X, None
 
 
-def candidate_configs(F, dtype, quick=False):
-    base = geot.geot_select_config(1 << 20, 1 << 16, F, "sum", torch.float32 if dtype == "f32" else torch.bfloat16)
+STREAM_PIPES = {1: [(16, 6, 4), (8, 6, 8), (16, 3, 8), (8, 8, 6)], 2: [(16, 3, 4), (8, 3, 8)], 4: [(8, 3, 4)],
+                8: [(8, 1, 4), (8, 1, 6)]}
+
+
+def candidate_configs(E, S, F, dtype, fused, quick=False):
+    tdt = torch.float32 if dtype == "f32" else torch.bfloat16
+    base = geot.geot_select_config(E, S, F, "sum", tdt, torch.int32, fused)
     out = []
-    Rs = [4, 8, 16, 32, 64] if not quick else [8, 32]
-    ctas = [0, 1, 2] if not quick else [0]
+    Rs = [8, 16, 32, 64] if not quick else [16, 64]
+    ctas = [0, 2] if not quick else [0]
     for R, c in itertools.product(Rs, ctas):
-        out.append({"rows_per_group": R, "ctas_per_sm": c})
+        out.append({"variant": 1, "rows_per_group": R, "ctas_per_sm": c})
+    if base.variant == 3:
+        for (w, rs, ns) in STREAM_PIPES.get(base.vecs_per_lane, []):
+            if rs <= base.lanes_per_row:
+                out.append({"variant": 3, "warps_per_cta": w, "rows_per_group": rs, "stages": ns})
     return base, out
 
 
@@ -92,7 +101,7 @@ def run(args):
         B = E * F * esz + E * 4 * (2 if fused else 1) + S * F * esz
         small = B < 4 * L2_BYTES
         out = torch.empty((S, F), dtype=X.dtype, device=dev)
-        base, cands = candidate_configs(F, dtype, args.quick)
+        base, cands = candidate_configs(E, S, F, dtype, fused, args.quick)
         maxlen = int(L.max())
         for cfg in cands:
             if fused:
