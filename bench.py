@@ -214,6 +214,10 @@ def run_ours(args):
     out = torch.empty((S, F), dtype=tdt, device=dev)
     B_rank = algorithmic_bytes(E, S, F, esz, 4)
     cfg = geot.geot_select_config(E, S, F, "sum", tdt, torch.int32, False)
+    user_cfg = json.loads(args.cfg) if args.cfg else None  # experiments only (selector override)
+    if user_cfg:
+        for k, v in user_cfg.items():
+            setattr(cfg, k, int(v))
     stream = torch.cuda.current_stream(dev)
 
     L_ = _lib.load()
@@ -223,7 +227,7 @@ def run_ours(args):
         prof.restype = None
 
     def step():
-        geot.geot_segment_reduce(X, idx, S, "sum", out=out, seg_base=s0)
+        geot.geot_segment_reduce(X, idx, S, "sum", out=out, seg_base=s0, cfg=user_cfg)
 
     def barrier():
         if N > 1:
@@ -350,6 +354,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-budget", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cfg", default="", help="JSON geot_config override (experiments; default = the selector)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
