@@ -191,7 +191,7 @@ def run_ours(args):
     torch.cuda.set_device(dev)
     import paper_2404_03019_b200 as geot
     import synth.device as sd
-    from paper_2404_03019_b200 import _lib
+    from paper_2404_03019_b200 import _lib, shard
 
     w = synth.workload(args.workload)
     Eg, Sg, F = w["E"] * N, w["S"] * N, w["F"]
@@ -203,7 +203,7 @@ def run_ours(args):
     if N > 1:
         gidx = sd.expand_index(bounds, 0, Eg, torch.int32)
         sb, eb = [b.cpu().numpy() for b in geot.geot_partition(gidx, Sg, N)]
-        e0, e1, s0, s1 = int(eb[rank]), int(eb[rank + 1]), int(sb[rank]), int(sb[rank + 1])
+        e0, e1, s0, s1 = shard.shard_of(sb, eb, rank)
         idx = gidx[e0:e1].clone()
         del gidx
     else:
@@ -259,15 +259,26 @@ def run_ours(args):
     kern_ms = None
     if prof is not None:
         kern_ms = statistics.mean(a.elapsed_time(b) for a, b in kev)
-    t = torch.tensor([ms, kern_ms if kern_ms is not None else ms], dtype=torch.float64, device=dev)
+    t = [ms, kern_ms if kern_ms is not None else ms]
     if N > 1:
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        tot = torch.tensor([B_rank, E * F], dtype=torch.float64, device=dev)
-        torch.distributed.all_reduce(tot)
-        B_all, EF_all = float(tot[0]), float(tot[1])
+        t = shard.max_over_ranks(t)
+        B_all, EF_all = shard.sum_over_ranks([B_rank, E * F])
     else:
         B_all, EF_all = float(B_rank), float(E * F)
     ms, kern_ms_max = float(t[0]), float(t[1])
+    ag_ms = None
+    if N > 1 and args.allgather:  # optional output all-gather (COLL-0), timed separately
+        for _ in range(2):
+            shard.allgather_rows(out, sb)
+        torch.cuda.synchronize()
+        barrier()
+        ga, gb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ga.record(stream)
+        for _ in range(5):
+            shard.allgather_rows(out, sb)
+        gb.record(stream)
+        torch.cuda.synchronize()
+        ag_ms = shard.max_over_ranks([ga.elapsed_time(gb) / 5])[0]
     value = B_all / (ms * 1e-3) / 1e9
     peak, peak_src = peaks()
 
@@ -333,6 +344,7 @@ def run_ours(args):
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "selected_config": cfg.as_dict(),
+        "allgather_ms": ag_ms,
     }
     if N == 1 and not args.no_cpu_baseline:
         v, cores, sample, _ = cpu_oracle_time(w, budget_s=args.cpu_budget)
@@ -355,6 +367,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cfg", default="", help="JSON geot_config override (experiments; default = the selector)")
+    ap.add_argument("--allgather", action="store_true", help="N>1: also time the optional output all-gather")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -1,0 +1,62 @@
+"""Multi-GPU host logic (H9): segment-boundary shards, the
+max-over-ranks step time, and the optional output all-gather.
+
+The reduction itself needs no collective: rank p owns output rows
+[s_p, s_{p+1}) and edges [e_p, e_{p+1}) of the partition computed by
+`geot_partition` (include/geot.h), and reduces them with `seg_base = s_p`.
+torch.distributed (NCCL on GPUs, gloo in the CPU tests) carries only the
+barrier, the max-over-ranks time and — optionally, timed separately — the
+all-gather of the output rows.  Pure host code: imports no kernel library.
+"""
+from __future__ import annotations
+
+from typing import Sequence
+
+
+def shard_of(seg_bounds: Sequence[int], edge_bounds: Sequence[int], rank: int):
+    """(e0, e1, s0, s1): the edge range and output-row range rank `rank` owns."""
+    P = len(seg_bounds) - 1
+    if not 0 <= rank < P or len(edge_bounds) != P + 1:
+        raise ValueError("rank out of range or bounds of different length")
+    e0, e1 = int(edge_bounds[rank]), int(edge_bounds[rank + 1])
+    s0, s1 = int(seg_bounds[rank]), int(seg_bounds[rank + 1])
+    if e1 < e0 or s1 < s0:
+        raise ValueError("bounds must be non-decreasing")
+    return e0, e1, s0, s1
+
+
+def max_over_ranks(values, group=None):
+    """Element-wise max of a list of floats over all ranks (timing rule)."""
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+    t = torch.tensor([float(v) for v in values], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return [float(v) for v in t.tolist()]
+
+
+def sum_over_ranks(values, group=None):
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+    t = torch.tensor([float(v) for v in values], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, group=group)
+    return [float(v) for v in t.tolist()]
+
+
+def allgather_rows(local_out, seg_bounds: Sequence[int], group=None):
+    """Assemble the full [S, F] output on every rank from the ranks' row blocks
+    (rank p holds rows [s_p, s_{p+1})).  Row counts differ per rank, so blocks
+    are padded to the largest and trimmed after one all_gather (COLL-0, the
+    optional collective of the north_star; NCCL over NVLink on GPUs)."""
+    import torch
+    import torch.distributed as dist
+    P = len(seg_bounds) - 1
+    counts = [int(seg_bounds[p + 1]) - int(seg_bounds[p]) for p in range(P)]
+    m = max(counts) if counts else 0
+    F = local_out.shape[1]
+    pad = torch.zeros((m, F), dtype=local_out.dtype, device=local_out.device)
+    pad[: local_out.shape[0]] = local_out
+    parts = [torch.empty_like(pad) for _ in range(P)]
+    dist.all_gather(parts, pad, group=group)
+    return torch.cat([parts[p][: counts[p]] for p in range(P)], dim=0)
