@@ -9,6 +9,7 @@
 
 #include "../../include/geot.h"
 #include "launch.cuh"
+#include "narrow.cuh"
 #include "select.h"
 
 namespace geot {
@@ -152,8 +153,20 @@ static geot_status resolve_config(long long nnz, long long S, long long F, geot_
     if (st != GEOT_OK) return st;
     if (user) {
         if (user->reserved != 0) return GEOT_ERR_INVALID_VALUE;
-        if (user->variant && user->variant != GEOT_VARIANT_EDGE_TILE && user->variant != GEOT_VARIANT_STREAM)
-            return GEOT_ERR_UNSUPPORTED;
+        if (user->variant < 0 || user->variant > GEOT_VARIANT_STREAM) return GEOT_ERR_UNSUPPORTED;
+        if (user->variant == GEOT_VARIANT_NARROW) {  // no tunables: the shape follows F
+            if (!narrow_eligible(nnz, F, dt, fused)) return GEOT_ERR_UNSUPPORTED;
+            c.variant = GEOT_VARIANT_NARROW;
+            *out = c;
+            return GEOT_OK;
+        }
+        const bool tile_fields = user->vec_elems || user->lanes_per_row || user->vecs_per_lane ||
+                                 user->rows_per_group || user->ctas_per_sm;
+        if (user->variant == GEOT_VARIANT_AUTO && c.variant == GEOT_VARIANT_NARROW && tile_fields) {
+            c.variant = GEOT_VARIANT_EDGE_TILE;  // edge-tile fields given: tune the edge-tile kernel
+            select_shape_for_vw(F, dt, &c);
+            c.ctas_per_sm = 0;
+        }
         if (user->variant == GEOT_VARIANT_EDGE_TILE && c.variant != GEOT_VARIANT_EDGE_TILE) {
             // back to the edge-tile defaults before applying the overrides
             c.variant = GEOT_VARIANT_EDGE_TILE;
@@ -251,6 +264,32 @@ static geot_status reduce_common(const void* X, long long V, const void* src_idx
         select_shape_for_vw(F, dt, &c);
     }
     unsigned char* wsb = static_cast<unsigned char*>(ws);
+    if (c.variant == GEOT_VARIANT_NARROW) {
+        if (mode == 0 && aligned(X, 16) && aligned(idx, 16)) {
+            const int nsm = sm_count();
+            const WsLayout L = ws_layout(narrow_agents_max(nsm), F);
+            if (!ws) return GEOT_ERR_INVALID_VALUE;
+            if (ws_bytes < L.total) return GEOT_ERR_WORKSPACE_TOO_SMALL;
+            NarrowParams np{};
+            np.X = X;
+            np.idx = idx;
+            np.out = out;
+            np.carry_h = reinterpret_cast<float*>(wsb + L.carry_h);
+            np.carry_t = reinterpret_cast<float*>(wsb + L.carry_t);
+            np.meta = reinterpret_cast<TileMeta*>(wsb + L.meta);
+            np.flag = reinterpret_cast<unsigned long long*>(wsb + L.flags);
+            np.ctrl = reinterpret_cast<StreamCtrl*>(wsb + L.ctrl);
+            np.E = nnz;
+            np.seg_base = seg_base;
+            np.S = S;
+            np.op = (int)op;
+            cudaError_t e = launch_narrow(np, (int)F, dt == GEOT_BF16, op == GEOT_MAX, it == GEOT_I64, nsm, stream);
+            if (e != cudaErrorNotSupported) return from_cuda(e);
+        } else if (user_cfg && user_cfg->variant == GEOT_VARIANT_NARROW) {
+            return GEOT_ERR_UNSUPPORTED;
+        }
+        c.variant = GEOT_VARIANT_EDGE_TILE;  // not applicable here: edge-tile kernel
+    }
     if (c.variant == GEOT_VARIANT_STREAM) {
         const int nsm = sm_count();
         const long long NA = stream_agents(nnz, c.lanes_per_row, c.warps_per_cta, nsm);
@@ -396,6 +435,11 @@ size_t geot_workspace_size(int64_t nnz, int64_t num_segments, int64_t F, geot_re
         select_shape_for_vw(F, dtype, &c2);  // its edge-tile fallback shape
         nt = std::max(nt, ntiles_of(nnz, c2));
         nt = std::max(nt, stream_agents(nnz, c.lanes_per_row, 16, sm_count()));  // 16 warps: the most agents
+    } else if (c.variant == GEOT_VARIANT_NARROW) {
+        geot_config c2 = c;
+        select_shape_for_vw(F, dtype, &c2);  // its edge-tile fallback shape
+        nt = std::max(nt, ntiles_of(nnz, c2));
+        nt = std::max(nt, narrow_agents_max(sm_count()));
     } else {
         nt = std::max(nt, ntiles_of(nnz, c));
     }

@@ -166,6 +166,11 @@ cudaError_t launch_stream(const StreamParams& p, const EdgeTileParams& fix, int 
 #undef GEOT_SSHAPE
     return cudaErrorNotSupported;
 }
+// small-F kernel family (inst_narrow.cu)
+struct NarrowParams;
+cudaError_t launch_narrow(const NarrowParams& p, int F, bool bf16, bool ismax, bool i64, int nsm, cudaStream_t st);
+long long narrow_agents_max(int nsm);
+
 cudaError_t launch_stream_f32(const StreamParams&, const EdgeTileParams&, int, int, int, int, int, bool, int, cudaStream_t);
 cudaError_t launch_stream_bf16(const StreamParams&, const EdgeTileParams&, int, int, int, int, int, bool, int, cudaStream_t);
 

@@ -16,5 +16,6 @@ void select_shape_for_vw(long long F, geot_dtype dt, geot_config* c);
 // GEOT_VARIANT_STREAM applicability and its rows per ring stage.
 bool stream_eligible(long long nnz, long long F, geot_dtype dt, int fused, const geot_config& c);
 int stream_rows_per_stage(long long F, geot_dtype dt, int lpr, int vpl);
+bool narrow_eligible(long long nnz, long long F, geot_dtype dt, int fused);
 
 }  // namespace geot

@@ -150,6 +150,31 @@ def test_stream_stress(geot, kind, F):
         parity(geot, 100_000, 9_000, F, op, "f32", "int", kind, seed=2, cfg=cfg)
 
 
+NARROW = 2  # GEOT_VARIANT_NARROW
+
+
+@pytest.mark.parametrize("F,dtype", [(1, "f32"), (2, "f32"), (4, "f32"), (8, "f32"), (1, "bf16"), (2, "bf16"),
+                                     (4, "bf16"), (8, "bf16"), (16, "bf16")])
+@pytest.mark.parametrize("op", ["sum", "mean", "max"])
+def test_narrow_variant(geot, F, dtype, op):
+    for mode in ("real", "int"):
+        parity(geot, 200_003, 200_003 // 9, F, op, dtype, mode, "powerlaw15", seed=F + 7, cfg={"variant": NARROW})
+
+
+@pytest.mark.parametrize("kind", synth.STRESS_KINDS)
+@pytest.mark.parametrize("itype", ["i32", "i64"])
+def test_narrow_stress(geot, kind, itype):
+    for F in (1, 4):
+        for op in ("sum", "mean", "max"):
+            parity(geot, 150_001, 12_000, F, op, "f32", "int", kind, seed=5, itype=itype, cfg={"variant": NARROW})
+
+
+def test_narrow_is_default_for_small_f(geot):
+    for F in (1, 2, 4, 8):
+        assert geot.geot_select_config(1 << 24, 1 << 20, F, "sum").variant == NARROW
+    parity(geot, 1 << 20, 1 << 16, 1, "sum", "f32", "real", "uniform", seed=9)
+
+
 def test_stream_int64_and_shards(geot):
     parity(geot, 300_000, 20_000, 64, "sum", "f32", "real", "powerlaw", seed=4, itype="i64", cfg={"variant": STREAM})
     L, idx, X = make_case(300_000, 20_000, 128, "f32", "int", "powerlaw15", 5)
