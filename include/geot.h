@@ -136,6 +136,17 @@ void geot_profile_events(cudaEvent_t before, cudaEvent_t after);
 geot_status geot_select_config(int64_t nnz, int64_t num_segments, int64_t F, geot_reduce op,
                                geot_dtype dtype, geot_itype itype, int fused, geot_config* cfg_out);
 
+/* The generated decision tree alone (select_tree.inc; Listing 5,
+ * P:432-444), for diagnostics and the codegen-fidelity test: leaf tuple
+ * (variant, rows_per_group, warps_per_cta, stages) for features
+ * log2(nnz), avg = nnz/num_segments, F, dtype (0 f32 / 1 bf16), fused (0/1);
+ * '<=' goes left at every threshold.  geot_select_config applies the leaf only
+ * where it is valid for the input (else the hand rules). */
+void geot_select_tree(double log2_nnz, double avg, double F, double dtype, double fused, int32_t out[4]);
+
+/* Provenance text of the compiled tree (perf DB, split, quality). */
+const char* geot_selector_provenance(void);
+
 /* Workspace (device bytes) the reduction needs for the given problem under
  * configuration *cfg (NULL = the configuration geot_select_config picks).
  * The workspace holds per-agent carries plus a few control words: it must be

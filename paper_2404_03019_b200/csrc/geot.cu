@@ -400,6 +400,14 @@ int geot_abi_version(void) { return GEOT_ABI_VERSION; }
 
 uint64_t geot_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
+void geot_select_tree(double log2_nnz, double avg, double F, double dtype, double fused, int32_t out[4]) {
+    int o[4];
+    select_tree_raw(log2_nnz, avg, F, dtype, fused, o);
+    for (int i = 0; i < 4; ++i) out[i] = o[i];
+}
+
+const char* geot_selector_provenance(void) { return select_tree_provenance(); }
+
 const char* geot_last_cuda_error(void) {
     return g_last_cuda_error == cudaSuccess ? "" : cudaGetErrorString(g_last_cuda_error);
 }

@@ -17,5 +17,10 @@ void select_shape_for_vw(long long F, geot_dtype dt, geot_config* c);
 bool stream_eligible(long long nnz, long long F, geot_dtype dt, int fused, const geot_config& c);
 int stream_rows_per_stage(long long F, geot_dtype dt, int lpr, int vpl);
 bool narrow_eligible(long long nnz, long long F, geot_dtype dt, int fused);
+bool stream_pipe_compiled(int lpr, int vpl, int w, int rs, int ns);
+
+// The generated tree itself (diagnostics / codegen-fidelity test) and its provenance.
+void select_tree_raw(double log2_nnz, double avg, double F, double dtype, double fused, int out[4]);
+const char* select_tree_provenance();
 
 }  // namespace geot

@@ -77,9 +77,11 @@ def candidate_configs(E, S, F, dtype, fused, quick=False):
     base = geot.geot_select_config(E, S, F, "sum", tdt, torch.int32, fused)
     out = []
     Rs = [8, 16, 32, 64] if not quick else [16, 64]
-    ctas = [0, 2] if not quick else [0]
+    ctas = [0] if not quick else [0]
     for R, c in itertools.product(Rs, ctas):
         out.append({"variant": 1, "rows_per_group": R, "ctas_per_sm": c})
+    if base.variant == 2:
+        out.append({"variant": 2})
     if base.variant == 3:
         for (w, rs, ns) in STREAM_PIPES.get(base.vecs_per_lane, []):
             if rs <= base.lanes_per_row:
@@ -125,7 +127,32 @@ def run(args):
 
 
 ARXIV = (1_166_243, 169_343)
+
+
+def selector_grid():
+    """Training/evaluation workloads of the selector refit (the B200 analog of the
+    paper's 51 datasets x augmentation): widths x sizes x mean degree."""
+    g = []
+    for F in (1, 2, 4, 8, 16, 32, 64, 128, 256, 512, 1024):
+        for logE in (18, 21, 24):
+            E = 1 << logE
+            if E * F * 4 > (6 << 30):
+                continue
+            for avg in (3, 16, 64):
+                g.append((E, max(1, E // avg), F, "f32", "powerlaw", "sum", False))
+    for F in (8, 64, 128, 256):
+        for logE in (20, 23):
+            g.append((1 << logE, (1 << logE) // 16, F, "bf16", "powerlaw", "sum", False))
+    for F in (4, 64, 128):
+        g.append((1 << 22, (1 << 22) // 16, F, "f32", "uniform", "sum", False))
+    for F in (16, 64, 128):
+        for avg in (8, 64):
+            g.append((1 << 23, (1 << 23) // avg, F, "f32", "powerlaw", "sum", True))
+    return g
+
+
 GRIDS = {
+    "selector": selector_grid(),
     "arxiv": [(ARXIV[0], ARXIV[1], 128, "f32", "powerlaw", "sum", False)],
     "main": [
         (ARXIV[0], ARXIV[1], 128, "f32", "powerlaw", "sum", False),
