@@ -336,7 +336,8 @@ def run_ours(args):
         "pct_of_peak": round(100 * value / (N * peak), 2), "edges_F_per_s": EF_all / (ms * 1e-3),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
-                     "kernel": "edge_tile_kernel (+ carry_fixup_kernel in the step)",
+                     "kernel": {1: "edge_tile_kernel (+ carry_fixup_kernel)", 2: "narrow_kernel",
+                                3: "stream_kernel"}.get(cfg.variant, "?"),
                      "kernel_ms": round(kern_ms_max, 5) if kern_ms is not None else None,
                      "algorithmic_bytes_per_launch": kern_bytes},
         "e2e": {"value": round(B_all / (e2e_ms * 1e-3) / 1e9, 3), "unit": UNIT, "h2d_bytes_per_step": h2d,

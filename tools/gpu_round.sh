@@ -10,6 +10,6 @@ timeout 300 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_
 cat gpurun_out/${TAG}_bench.json; tail -3 gpurun_out/${TAG}_bench.err
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/${TAG}_launches.csv \
    python bench.py --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 1 > /dev/null 2>&1; echo "ncu-list rc=$?"
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:edge_tile -s 5 -c 1 -o gpurun_out/${TAG}_prof \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"stream_kernel|edge_tile" -s 5 -c 1 -o gpurun_out/${TAG}_prof \
    python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/${TAG}_ncu_full.log 2>&1; echo "ncu-full rc=$?"
 tail -3 gpurun_out/${TAG}_ncu_full.log
