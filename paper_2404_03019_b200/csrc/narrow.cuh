@@ -127,6 +127,7 @@ __global__ void __launch_bounds__(kNarrowWarps * 32) narrow_kernel(const NarrowP
         for (int f = 0; f < F; ++f) st_elem<T>(row + f, finalize(v[f], p.op, count));
     };
     auto gap_fill = [&](long long lo_k, long long hi_k) {  // rows strictly between two keys
+        if (hi_k <= lo_k + 1) return;  // the common case: adjacent (or unsorted) keys, no gap
         long long r0 = (lo_k < seg_lo) ? seg_lo : lo_k + 1;
         long long r1 = (hi_k > seg_hi) ? seg_hi : hi_k;
         for (long long r = r0; r < r1; ++r)
@@ -171,7 +172,7 @@ __global__ void __launch_bounds__(kNarrowWarps * 32) narrow_kernel(const NarrowP
         int nv = (int)min((long long)ITEMS, e_hi - r0);     // valid items (may be <= 0)
         if (nv < 0) nv = 0;
         float v[ITEMS][F];
-        long long k[ITEMS];
+        IdxT k[ITEMS];  // 32-bit keys for int32 indices (cheaper compares)
         if (nv == ITEMS) {  // full lane: vector loads (ITEMS-aligned rows => aligned bytes)
             uint32_t vw[VWORDS], kw[KWORDS];
 #pragma unroll
@@ -186,15 +187,15 @@ __global__ void __launch_bounds__(kNarrowWarps * 32) narrow_kernel(const NarrowP
                 if constexpr (I64)
                     k[i] = (long long)(((unsigned long long)kw[2 * i + 1] << 32) | kw[2 * i]);
                 else
-                    k[i] = (long long)(int)kw[i];
+                    k[i] = (int)kw[i];
             }
         } else {
 #pragma unroll
             for (int i = 0; i < ITEMS; ++i) {
                 const bool ok = i < nv;
 #pragma unroll
-                for (int f = 0; f < F; ++f) v[i][f] = ok ? ld_elem<T>(X + (r0 + i) * F + f) : 0.f;
-                k[i] = ok ? key_at(r0 + i) : KEY_AFTER;
+                for (int f = 0; f < F; ++f) v[i][f] = ok ? ld_elem<T>(X + (r0 + i) * F + f) : identity<ISMAX>();
+                k[i] = ok ? __ldg(I + r0 + i) : (IdxT)0;  // items >= nv are never read
             }
         }
         // neighbours: last key of the previous lane (lane 0: the open segment's key)
@@ -222,48 +223,46 @@ __global__ void __launch_bounds__(kNarrowWarps * 32) narrow_kernel(const NarrowP
                 next_first = (nr < e_hi) ? key_at(nr) : nextk;
         }
 
-        // ---- lane-sequential pass (SR): head partial, inner segments, tail partial
-        float h[F], t[F];
-        ident(h);
-        ident(t);
-        bool boundary = false;   // an inner segment boundary exists in this lane
-        int tstart_item = 0;     // item where the lane's last segment starts
-        bool cont = nv > 0 && k[0] == prev_last;  // first segment continues from the left
-        if (nv > 0 && !cont) gap_fill(prev_last, k[0]);
+        // ---- lane pass (SR): an inclusive segmented scan over the lane's items,
+        // predicated (no per-item divergent branches): acc[i] = value of the
+        // segment containing item i from its start (or from the lane start if
+        // it began further left), st[i] = its start row relative to e_lo (-2:
+        // began left of this lane).  is_seg (Alg. 1): key differs from the left.
+        const int lane_rel = (int)(r0 - e_lo);
+        float acc[ITEMS][F];
+        int st[ITEMS];
+        bool head[ITEMS];
+        bool any_head = false;
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
-            if (i < nv) {
-                if (i > 0 && k[i] != k[i - 1]) {  // is_seg: segment k[i-1] ended at item i-1
-                    if (!boundary) {
-                        boundary = true;
+            head[i] = (i < nv) && ((i == 0) ? ((long long)k[0] != prev_last) : (k[i] != k[i - 1]));
+            any_head = any_head || head[i];
 #pragma unroll
-                        for (int f = 0; f < F; ++f) h[f] = t[f];  // first segment's lane part
-                    } else {  // a segment wholly inside the lane: write it now
-                        write_seg(k[i - 1], t, i - tstart_item);
-                    }
-                    gap_fill(k[i - 1], k[i]);
-                    tstart_item = i;
-                    ident(t);
-                }
-#pragma unroll
-                for (int f = 0; f < F; ++f) t[f] = fold<ISMAX>(t[f], v[i][f]);
-            }
+            for (int f = 0; f < F; ++f)
+                acc[i][f] = (i == 0 || head[i]) ? v[i][f] : fold<ISMAX>(acc[i - 1][f], v[i][f]);
+            st[i] = head[i] ? lane_rel + i : ((i == 0) ? -2 : st[i - 1]);
         }
-        if (!boundary) {
+        const bool cont = nv > 0 && !head[0];  // the first segment continues from the left
+        // gaps: rows strictly between a key and the next different one (rare:
+        // only where segments are empty) — filled by the lane holding the head
+        unsigned gaps = 0;  // heads whose key is not the previous key + 1
 #pragma unroll
-            for (int f = 0; f < F; ++f) h[f] = t[f];
+        for (int i = 0; i < ITEMS; ++i)
+            if (head[i] && (i == 0 ? (long long)k[0] != prev_last + 1 : (long long)k[i] != (long long)k[i - 1] + 1))
+                gaps |= 1u << i;
+        if (__any_sync(0xffffffffu, gaps != 0)) {
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i)
+                if ((gaps >> i) & 1u) gap_fill((i == 0) ? prev_last : (long long)k[i - 1], (long long)k[i]);
         }
 
-        // ---- warp segmented inclusive scan of tail partials (Alg. 1 analog)
-        // reset flag: the lane's last segment starts inside this lane
-        const bool starts = nv > 0 && (boundary || !cont);
+        // ---- warp segmented inclusive scan of the lane tails (Alg. 1 analog)
         float sv[F];
 #pragma unroll
-        for (int f = 0; f < F; ++f) sv[f] = t[f];
-        // segment start rows are kept relative to e_lo (32-bit); -2 = "inherit from
-        // the left" doubles as the scan's reset flag (a lane with a start resets)
-        const int lane_rel = (int)(r0 - e_lo);
-        int sst = starts ? lane_rel + tstart_item : -2;
+        for (int f = 0; f < F; ++f) sv[f] = acc[ITEMS - 1][f];
+        // -2 = "inherit from the left" doubles as the scan's reset flag
+        int sst = (nv > 0) ? st[ITEMS - 1] : -2;
+        (void)any_head;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
             float ov[F];
@@ -293,41 +292,31 @@ __global__ void __launch_bounds__(kNarrowWarps * 32) narrow_kernel(const NarrowP
             cst = rstart;
         }
 
-        // ---- writes: the first segment when it ends inside the lane ...
-        if (nv > 0 && boundary) {
-            float tot[F];
-            int st0;
-            if (cont) {
+        // ---- items before the lane's first head continue the segment from the left
 #pragma unroll
-                for (int f = 0; f < F; ++f) tot[f] = fold<ISMAX>(cin[f], h[f]);
-                st0 = cst;
-            } else {
+        for (int i = 0; i < ITEMS; ++i) {
+            if (cont && st[i] == -2) {
 #pragma unroll
-                for (int f = 0; f < F; ++f) tot[f] = h[f];
-                st0 = lane_rel;
-            }
-            // first segment ends at the item before the first inner boundary
-            int b1 = 1;
-#pragma unroll
-            for (int i = ITEMS - 1; i >= 1; --i)
-                if (i < nv && k[i] != k[i - 1]) b1 = i;
-            if (st0 == -1) {  // began in an earlier agent: this agent owns it (resolved below)
-#pragma unroll
-                for (int f = 0; f < F; ++f) hacc[f] = tot[f];
-                head_end = r0 + b1;
-            } else {
-                write_seg(k[0], tot, lane_rel + b1 - st0);
+                for (int f = 0; f < F; ++f) acc[i][f] = fold<ISMAX>(cin[f], acc[i][f]);
+                st[i] = cst;
             }
         }
-        // ... and the last segment when the next row starts another segment
+        // ---- writes: every item that ends a segment stores it (predicated, once)
         const bool last_ends = nv > 0 && next_first != my_last;
-        if (last_ends) {
-            if (sst == -1) {
 #pragma unroll
-                for (int f = 0; f < F; ++f) hacc[f] = sv[f];
-                head_end = r0 + nv;
-            } else {
-                write_seg(my_last, sv, lane_rel + nv - sst);
+        for (int i = 0; i < ITEMS; ++i) {
+            const bool ends = (i < nv) && ((i + 1 < nv) ? head[i + 1] : (i == nv - 1 && last_ends));
+            if (ends && st[i] == -1) {  // began in an earlier agent: this agent owns it (below)
+#pragma unroll
+                for (int f = 0; f < F; ++f) hacc[f] = acc[i][f];
+                head_end = r0 + i + 1;
+            }
+            const long long key = (long long)k[i];
+            if (ends && st[i] != -1 && key >= seg_lo && key < seg_hi) {  // predicated store
+                T* row = out + (key - seg_lo) * F;
+                const int cnt = lane_rel + i + 1 - st[i];
+#pragma unroll
+                for (int f = 0; f < F; ++f) st_elem<T>(row + f, finalize(acc[i][f], p.op, cnt));
             }
         }
         // ---- running segment for the next chunk: the last valid lane's scan value
