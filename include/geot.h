@@ -208,6 +208,32 @@ geot_status geot_gather_segment_reduce_ex(const void* x, int64_t num_x_rows, con
                                           geot_dtype dtype, geot_itype itype, void* out, void* workspace,
                                           size_t ws_bytes, const geot_config* cfg, cudaStream_t stream);
 
+/* f3 (the paper defers autograd: P:497):
+ * gradient of geot_segment_reduce (seg_base 0) w.r.t. src:
+ *   grad_src[e,:] = g * grad_out[idx[e],:]  with g = 1 (sum), 1/count (mean),
+ *   [src[e,f] == out[s,f]] / ties[s,f] (max; ties split evenly).
+ *   grad_out  [num_segments, F] (dtype), device
+ *   offsets   [num_segments+1] int64 from geot_segment_offsets (mean; else NULL)
+ *   src, out  the forward input / output (max; else NULL)
+ *   ties      [num_segments, F] fp32 scratch (max; else NULL)
+ *   grad_src  [nnz, F] (dtype), device, write-only.  Deterministic. */
+geot_status geot_segment_reduce_backward(const void* grad_out, const void* idx, int64_t nnz, int64_t num_segments,
+                                         int64_t F, geot_reduce op, geot_dtype dtype, geot_itype itype,
+                                         const int64_t* offsets, const void* src, const void* out, float* ties,
+                                         void* grad_src, cudaStream_t stream);
+
+/* f3: gradients of the (weighted) fused form, fp32, op sum or mean:
+ *   grad_x[v,:]  = sum_{e: src[e]==v} w[e] * g(e) * grad_out[dst[e],:]   (scatter by the
+ *                  unsorted source index: fp32 atomics, NOT bitwise reproducible)
+ *   grad_w[e]    = g(e) * <x[src[e],:], grad_out[dst[e],:]>              (SDDMM)
+ * with g = 1 (sum) or 1/count[dst[e]] (mean; offsets from geot_segment_offsets).
+ * weight / grad_x / grad_w / x nullable (grad_w needs x). */
+geot_status geot_gather_segment_reduce_backward(const float* grad_out, const void* src_idx, const void* dst_idx,
+                                                const float* weight, int64_t nnz, int64_t num_segments,
+                                                int64_t num_x_rows, int64_t F, geot_reduce op, geot_itype itype,
+                                                const int64_t* offsets, const float* x, float* grad_x, float* grad_w,
+                                                cudaStream_t stream);
+
 /* H3: segment offsets (CSR row pointer) of a sorted index:
  *   offsets[s] = #{ e : idx[e] < s },  s = 0..num_segments  (int64, device,
  *   num_segments + 1 entries, write-only).  counts[s] = offsets[s+1]-offsets[s].

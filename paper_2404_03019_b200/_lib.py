@@ -66,6 +66,10 @@ SIGNATURES = {
     "geot_gather_segment_reduce_ex": ([_vp, _i64, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i32, _i32, _i32, _vp,
                                        _vp, _sz, _cfgp, _vp], _i32),
     "geot_segment_offsets": ([_vp, _i32, _i64, _i64, _vp, _vp], _i32),
+    "geot_segment_reduce_backward": ([_vp, _vp, _i64, _i64, _i64, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp],
+                                     _i32),
+    "geot_gather_segment_reduce_backward": ([_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i32, _i32, _vp, _vp, _vp,
+                                             _vp, _vp], _i32),
     "geot_validate_index": ([_vp, _i32, _i64, _i64, _vp, _i64, _vp, _vp], _i32),
     "geot_partition": ([_vp, _i32, _i64, _i64, _i32, _vp, _vp, _vp], _i32),
 }

@@ -500,6 +500,51 @@ geot_status geot_gather_segment_reduce_ex(const void* x, int64_t num_x_rows, con
                          out, workspace, ws_bytes, cfg, stream, weight ? 2 : 1);
 }
 
+geot_status geot_segment_reduce_backward(const void* grad_out, const void* idx, int64_t nnz, int64_t num_segments,
+                                         int64_t F, geot_reduce op, geot_dtype dtype, geot_itype itype,
+                                         const int64_t* offsets, const void* src, const void* out, float* ties,
+                                         void* grad_src, cudaStream_t stream) {
+    geot_status st = check_enums(op, dtype, itype);
+    if (st != GEOT_OK) return st;
+    if (nnz < 0 || num_segments < 0 || F < 1) return GEOT_ERR_INVALID_VALUE;
+    if (nnz == 0) return GEOT_OK;
+    if (!grad_out || !idx || !grad_src) return GEOT_ERR_INVALID_VALUE;
+    if (op == GEOT_MEAN && !offsets) return GEOT_ERR_INVALID_VALUE;
+    if (op == GEOT_MAX && (!src || !out || !ties)) return GEOT_ERR_INVALID_VALUE;
+    cudaError_t e = launch_segment_backward(grad_out, idx, itype == GEOT_I64, nnz, 0, num_segments, (int)F, (int)op,
+                                            dtype == GEOT_BF16, reinterpret_cast<const long long*>(offsets), src, out,
+                                            ties, grad_src, stream);
+    if (e == cudaSuccess) g_launches.fetch_add(op == GEOT_MAX ? 2 : 1, std::memory_order_relaxed);
+    return from_cuda(e);
+}
+
+geot_status geot_gather_segment_reduce_backward(const float* grad_out, const void* src_idx, const void* dst_idx,
+                                                const float* weight, int64_t nnz, int64_t num_segments,
+                                                int64_t num_x_rows, int64_t F, geot_reduce op, geot_itype itype,
+                                                const int64_t* offsets, const float* x, float* grad_x, float* grad_w,
+                                                cudaStream_t stream) {
+    if ((int)itype < 0 || (int)itype > 1) return GEOT_ERR_INVALID_VALUE;
+    if (op != GEOT_SUM && op != GEOT_MEAN) return GEOT_ERR_UNSUPPORTED;
+    if (nnz < 0 || num_segments < 0 || num_x_rows < 0 || F < 1) return GEOT_ERR_INVALID_VALUE;
+    if (op == GEOT_MEAN && !offsets) return GEOT_ERR_INVALID_VALUE;
+    if (grad_w && !x) return GEOT_ERR_INVALID_VALUE;
+    const long long* off = reinterpret_cast<const long long*>(offsets);
+    if (grad_x) {
+        if (!grad_out || (nnz > 0 && (!src_idx || !dst_idx))) return GEOT_ERR_INVALID_VALUE;
+        cudaError_t e = launch_gather_backward_x(grad_out, src_idx, dst_idx, itype == GEOT_I64, weight, nnz, 0,
+                                                 num_segments, num_x_rows, (int)F, (int)op, off, grad_x, stream);
+        if (e != cudaSuccess) return from_cuda(e);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+    }
+    if (grad_w && nnz > 0) {
+        cudaError_t e = launch_sddmm(x, grad_out, src_idx, dst_idx, itype == GEOT_I64, nnz, 0, num_segments,
+                                     num_x_rows, (int)F, (int)op, off, grad_w, stream);
+        if (e != cudaSuccess) return from_cuda(e);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+    }
+    return GEOT_OK;
+}
+
 geot_status geot_segment_offsets(const void* idx, geot_itype itype, int64_t nnz, int64_t num_segments,
                                  int64_t* offsets, cudaStream_t stream) {
     if ((int)itype < 0 || (int)itype > 1) return GEOT_ERR_INVALID_VALUE;

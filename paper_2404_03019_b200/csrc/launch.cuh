@@ -166,6 +166,17 @@ cudaError_t launch_stream(const StreamParams& p, const EdgeTileParams& fix, int 
 #undef GEOT_SSHAPE
     return cudaErrorNotSupported;
 }
+// gradients (backward.cu)
+cudaError_t launch_segment_backward(const void* dY, const void* idx, int idx64, long long E, long long seg_base,
+                                    long long S, int F, int op, int bf16, const long long* offsets, const void* X,
+                                    const void* Y, float* ties, void* dX, cudaStream_t st);
+cudaError_t launch_gather_backward_x(const float* dY, const void* src, const void* dst, int idx64, const float* w,
+                                     long long E, long long seg_base, long long S, long long V, int F, int op,
+                                     const long long* offsets, float* dx, cudaStream_t st);
+cudaError_t launch_sddmm(const float* x, const float* dY, const void* src, const void* dst, int idx64, long long E,
+                         long long seg_base, long long S, long long V, int F, int op, const long long* offsets,
+                         float* dw, cudaStream_t st);
+
 // small-F kernel family (inst_narrow.cu)
 struct NarrowParams;
 cudaError_t launch_narrow(const NarrowParams& p, int F, bool bf16, bool ismax, bool i64, int nsm, cudaStream_t st);

@@ -76,15 +76,22 @@ def candidate_configs(E, S, F, dtype, fused, quick=False):
     tdt = torch.float32 if dtype == "f32" else torch.bfloat16
     base = geot.geot_select_config(E, S, F, "sum", tdt, torch.int32, fused)
     out = []
-    Rs = [8, 16, 32, 64] if not quick else [16, 64]
+    Rs = ([2, 4] if E < 100_000 else []) + ([8, 16, 32, 64] if not quick else [16, 64])
     ctas = [0] if not quick else [0]
     for R, c in itertools.product(Rs, ctas):
         out.append({"variant": 1, "rows_per_group": R, "ctas_per_sm": c})
-    if base.variant == 2:
+    # eligibility from the input alone (not from the current selection)
+    esz = 4 if dtype == "f32" else 2
+    narrow_ok = (not fused) and E >= 65536 and (F in (1, 2, 4, 8) or (dtype == "bf16" and F == 16))
+    nv = F * esz // 16 if (F * esz) % 16 == 0 else 0
+    lpr = 32 if nv >= 32 else (1 << max(0, (nv - 1).bit_length())) if nv else 0
+    vpl = 1 if nv <= 32 else min(8 if dtype == "f32" else 4, 1 << ((nv + 31) // 32 - 1).bit_length())
+    stream_ok = (not fused) and E >= 65536 and nv > 0 and lpr >= 8 and nv <= lpr * vpl
+    if narrow_ok:
         out.append({"variant": 2})
-    if base.variant == 3:
-        for (w, rs, ns) in STREAM_PIPES.get(base.vecs_per_lane, []):
-            if rs <= base.lanes_per_row:
+    if stream_ok:
+        for (w, rs, ns) in STREAM_PIPES.get(vpl, []):
+            if rs <= lpr:
                 out.append({"variant": 3, "warps_per_cta": w, "rows_per_group": rs, "stages": ns})
     return base, out
 
@@ -148,6 +155,15 @@ def selector_grid():
     for F in (16, 64, 128):
         for avg in (8, 64):
             g.append((1 << 23, (1 << 23) // avg, F, "f32", "powerlaw", "sum", True))
+    # small graphs (Cora/Citeseer/PubMed-sized) and arxiv-sized ones
+    for F in (8, 16, 32, 64, 128):
+        for E in (4096, 10_556, 40_000):
+            for avg in (3, 8):
+                g.append((E, max(1, E // avg), F, "f32", "powerlaw", "sum", False))
+    for F in (64, 128, 256):
+        for E in (600_000, 1_166_243, 2_500_000):
+            for avg in (4, 7, 20):
+                g.append((E, E // avg, F, "f32", "powerlaw", "sum", False))
     return g
 
 
