@@ -55,6 +55,11 @@ def lib():
         L.oracle_gather_segment_reduce.restype = i32
         L.oracle_partition.argtypes = [vp, i32, i64, i64, i32, vp, vp]
         L.oracle_partition.restype = i32
+        L.oracle_segment_reduce_backward.argtypes = [vp, vp, i32, vp, i32, i64, i64, i64, i32, vp]
+        L.oracle_segment_reduce_backward.restype = i32
+        L.oracle_gather_segment_reduce_backward.argtypes = [vp, vp, i64, vp, vp, i32, vp, i64, i64, i64, i32, vp,
+                                                            vp]
+        L.oracle_gather_segment_reduce_backward.restype = i32
         _lib = L
     return _lib
 
@@ -140,6 +145,39 @@ def gather_segment_reduce(x, src_idx, dst_idx, S, op="sum", weight=None, nthread
     if rc:
         raise ValueError("oracle_gather_segment_reduce rejected its arguments")
     return Result(y, a, r)
+
+
+def segment_reduce_backward(dY, X, idx, op="sum"):
+    """VJP of segment_reduce w.r.t. X (fp64): dX[e] = g * dY[idx[e]] (see the C header)."""
+    X, dt = _vals(X)
+    idx, it = _index(idx)
+    dY = np.ascontiguousarray(dY, dtype=np.float64)
+    S, F = dY.shape
+    dX = np.zeros((idx.shape[0], F), dtype=np.float64)
+    rc = lib().oracle_segment_reduce_backward(_ptr(dY), _ptr(X), dt, _ptr(idx), it, idx.shape[0], S, F, OPS[op],
+                                              _ptr(dX))
+    if rc:
+        raise ValueError("oracle_segment_reduce_backward rejected its arguments")
+    return dX
+
+
+def gather_segment_reduce_backward(dY, x, src_idx, dst_idx, op="sum", weight=None):
+    """(dx, dw) of the (weighted) fused form, fp64; x fp32."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    dst_idx, it = _index(dst_idx)
+    src_idx = np.ascontiguousarray(src_idx, dtype=dst_idx.dtype)
+    dY = np.ascontiguousarray(dY, dtype=np.float64)
+    S, F = dY.shape
+    V = x.shape[0]
+    E = dst_idx.shape[0]
+    w = None if weight is None else np.ascontiguousarray(weight, dtype=np.float32)
+    dx = np.zeros((V, F), dtype=np.float64)
+    dw = np.zeros(E, dtype=np.float64)
+    rc = lib().oracle_gather_segment_reduce_backward(_ptr(dY), _ptr(x), V, _ptr(src_idx), _ptr(dst_idx), it, _ptr(w),
+                                                     E, S, F, OPS[op], _ptr(dx), _ptr(dw))
+    if rc:
+        raise ValueError("oracle_gather_segment_reduce_backward rejected its arguments")
+    return dx, dw
 
 
 def partition(idx, S, nparts):

@@ -287,4 +287,67 @@ int oracle_partition(const void* idx, int itype, int64_t nnz, int64_t S, int npa
     return 0;
 }
 
+/* ---------------------------------------------------------------------------
+ * Gradients (the paper defers autograd):
+ * the derivative of the definition above, as a vector-Jacobian product with
+ * the output gradient dY (fp64, [S, F]):
+ *   sum : dX[e,f] = dY[s,f]                       (s = idx[e])
+ *   mean: dX[e,f] = dY[s,f] / count[s]
+ *   max : dX[e,f] = dY[s,f] / ties[s,f]  if X[e,f] == max_s,f  else 0
+ *         (ties split evenly — DESIGN.md reading R19)
+ * ------------------------------------------------------------------------- */
+int oracle_segment_reduce_backward(const double* dY, const void* X, int dtype, const void* idx, int itype,
+                                   int64_t nnz, int64_t S, int64_t F, int op, double* dX) {
+    if (nnz < 0 || S < 0 || F < 1) return -1;
+    int64_t* offsets = (int64_t*)malloc(sizeof(int64_t) * (size_t)(S + 1));
+    oracle_offsets(idx, itype, nnz, S, offsets);
+    for (int64_t s = 0; s < S; ++s) {
+        const int64_t e0 = offsets[s], e1 = offsets[s + 1];
+        for (int64_t f = 0; f < F; ++f) {
+            double mx = 0.0, ties = 0.0;
+            if (op == OR_MAX) {
+                for (int64_t e = e0; e < e1; ++e) {
+                    const double v = get_value(X, dtype, e * F + f);
+                    if (e == e0 || v > mx) mx = v;
+                }
+                for (int64_t e = e0; e < e1; ++e)
+                    if (get_value(X, dtype, e * F + f) == mx) ties += 1.0;
+            }
+            for (int64_t e = e0; e < e1; ++e) {
+                double g = dY[s * F + f];
+                if (op == OR_MEAN) g = g / (double)(e1 - e0);
+                if (op == OR_MAX) g = (get_value(X, dtype, e * F + f) == mx) ? g / ties : 0.0;
+                dX[e * F + f] = g;
+            }
+        }
+    }
+    free(offsets);
+    return 0;
+}
+
+/* Fused form (x fp32 [V, F]):  dx[v,f] = sum_{e: src[e]==v} w[e] * g(e) * dY[dst[e],f],
+ * dw[e] = g(e) * sum_f x[src[e],f] * dY[dst[e],f];  g = 1 (sum) or 1/count (mean). */
+int oracle_gather_segment_reduce_backward(const double* dY, const float* x, int64_t V, const void* src_idx,
+                                          const void* dst_idx, int itype, const float* w, int64_t nnz, int64_t S,
+                                          int64_t F, int op, double* dx, double* dw) {
+    if (nnz < 0 || S < 0 || F < 1 || V < 0 || op == OR_MAX) return -1;
+    int64_t* offsets = (int64_t*)malloc(sizeof(int64_t) * (size_t)(S + 1));
+    oracle_offsets(dst_idx, itype, nnz, S, offsets);
+    if (dx)
+        for (int64_t i = 0; i < V * F; ++i) dx[i] = 0.0;
+    for (int64_t e = 0; e < nnz; ++e) {
+        const int64_t s = get_index(dst_idx, itype, e), r = get_index(src_idx, itype, e);
+        double g = 1.0;
+        if (op == OR_MEAN) g = 1.0 / (double)(offsets[s + 1] - offsets[s]);
+        double dot = 0.0;
+        for (int64_t f = 0; f < F; ++f) {
+            if (dx) dx[r * F + f] += (w ? (double)w[e] : 1.0) * g * dY[s * F + f];
+            dot += (double)x[r * F + f] * dY[s * F + f];
+        }
+        if (dw) dw[e] = g * dot;
+    }
+    free(offsets);
+    return 0;
+}
+
 int oracle_abi_version(void) { return 1; }

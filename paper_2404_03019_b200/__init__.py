@@ -210,6 +210,84 @@ def geot_partition(idx, num_segments, nparts):
     return sb, eb
 
 
+def geot_segment_reduce_backward(grad_out, idx, op="sum", offsets=None, src=None, out=None, grad_src=None):
+    """Gradient w.r.t. src of geot_segment_reduce (seg_base 0); see include/geot.h."""
+    dev = _dev(grad_out, idx, offsets, src, out, grad_src)
+    S, F = grad_out.shape
+    E = idx.numel()
+    if grad_src is None:
+        grad_src = torch.empty((E, F), dtype=grad_out.dtype, device=dev)
+    if op == "mean" and offsets is None:
+        offsets = geot_segment_offsets(idx, S)
+    ties = torch.empty((S, F), dtype=torch.float32, device=dev) if op == "max" else None
+    with torch.cuda.device(dev):
+        _lib.check(_L.geot_segment_reduce_backward(_ptr(grad_out), _ptr(idx), E, S, F, _op(op), _dt(grad_out),
+                                                   _it(idx), _ptr(offsets), _ptr(src), _ptr(out), _ptr(ties),
+                                                   _ptr(grad_src), _stream(dev)), "geot_segment_reduce_backward")
+    return grad_src
+
+
+def geot_gather_segment_reduce_backward(grad_out, x, src_idx, dst_idx, op="sum", weight=None, offsets=None,
+                                        need_x=True, need_w=False):
+    """(grad_x, grad_weight) of the fused form (fp32); grad_x by fp32 atomics."""
+    dev = _dev(grad_out, x, src_idx, dst_idx, weight, offsets)
+    S, F = grad_out.shape
+    V = x.shape[0]
+    E = dst_idx.numel()
+    if op == "mean" and offsets is None:
+        offsets = geot_segment_offsets(dst_idx, S)
+    gx = torch.empty((V, F), dtype=torch.float32, device=dev) if need_x else None
+    gw = torch.empty(E, dtype=torch.float32, device=dev) if need_w else None
+    with torch.cuda.device(dev):
+        _lib.check(_L.geot_gather_segment_reduce_backward(_ptr(grad_out), _ptr(src_idx), _ptr(dst_idx),
+                                                          _ptr(weight), E, S, V, F, _op(op), _it(dst_idx),
+                                                          _ptr(offsets), _ptr(x), _ptr(gx), _ptr(gw), _stream(dev)),
+                   "geot_gather_segment_reduce_backward")
+    return gx, gw
+
+
+class _SegmentReduceFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, src, idx, num_segments, reduce):
+        out = geot_segment_reduce(src, idx, num_segments, reduce)
+        ctx.reduce = reduce
+        ctx.save_for_backward(idx, src if reduce == "max" else None, out if reduce == "max" else None)
+        return out
+
+    @staticmethod
+    def backward(ctx, grad_out):
+        idx, src, out = ctx.saved_tensors
+        g = geot_segment_reduce_backward(grad_out.contiguous(), idx, ctx.reduce, src=src, out=out)
+        return g, None, None, None
+
+
+class _GatherSegmentReduceFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, src_idx, dst_idx, weight, num_segments, reduce):
+        out = geot_gather_segment_reduce(x, src_idx, dst_idx, num_segments, reduce, weight=weight)
+        ctx.reduce = reduce
+        ctx.save_for_backward(x, src_idx, dst_idx, weight)
+        return out
+
+    @staticmethod
+    def backward(ctx, grad_out):
+        x, src_idx, dst_idx, weight = ctx.saved_tensors
+        need_w = weight is not None and ctx.needs_input_grad[3]
+        gx, gw = geot_gather_segment_reduce_backward(grad_out.contiguous(), x, src_idx, dst_idx, ctx.reduce,
+                                                     weight=weight, need_x=ctx.needs_input_grad[0], need_w=need_w)
+        return gx, None, None, gw, None, None
+
+
+def segment_reduce_autograd(idx, msg, reduce="sum", num_segments=None):
+    """segment_reduce with gradients w.r.t. msg (sum/mean/max)."""
+    return _SegmentReduceFn.apply(msg, idx, _num_segments(idx, num_segments), reduce)
+
+
+def index_segment_reduce_autograd(src_idx, dst_idx, x, reduce="sum", weight=None, num_segments=None):
+    """Fused form with gradients w.r.t. x (and weight): fp32, sum/mean."""
+    return _GatherSegmentReduceFn.apply(x, src_idx, dst_idx, weight, _num_segments(dst_idx, num_segments), reduce)
+
+
 # ------------------------------------------------------------ paper-style API
 def segment_reduce(idx, msg, reduce="sum", num_segments=None):
     """geot.segment_reduce(edge_index[1], msg, reduce=...)  — PAPER.md:289."""

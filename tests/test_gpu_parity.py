@@ -325,3 +325,50 @@ def test_device_generator_matches_host():
     np.testing.assert_array_equal(sd.index_from_lengths(L, torch.int64).cpu().numpy(), synth.lengths_to_index(L))
     np.testing.assert_array_equal(sd.src_index(5000, 977, 1234, e_begin=99).cpu().numpy(),
                                   synth.src_index(1234, 99, 5000, 977))
+
+
+# ---------------------------------------------------------------- gradients (f3)
+@pytest.mark.parametrize("op", ["sum", "mean", "max"])
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_segment_reduce_backward(geot, op, dtype):
+    mode = "int"
+    L, idx, X = make_case(30_000, 4_000, 16, dtype, mode, "gaps", seed=21)
+    rng = np.random.default_rng(3)
+    dY = rng.integers(-4, 5, size=(4_000, 16)).astype(np.float32)  # exact in bf16 too
+    ref = oracle.segment_reduce_backward(dY.astype(np.float64), X, idx, op)
+    xt = to_torch_vals(X).requires_grad_(True)
+    it = torch.from_numpy(idx).to(torch.int32).cuda()
+    y = geot.segment_reduce_autograd(it, xt, op, num_segments=4_000)
+    dyt = torch.from_numpy(dY).cuda().to(xt.dtype)
+    y.backward(dyt)
+    got = xt.grad.float().cpu().numpy().astype(np.float64)
+    want = ref
+    if dtype == "bf16":  # one RNE rounding of the fp32 gradient
+        want = torch.tensor(ref).float().bfloat16().float().numpy().astype(np.float64)
+    elif op != "sum":
+        want = ref.astype(np.float32).astype(np.float64)  # fp32 division, one rounding
+    np.testing.assert_array_equal(got, want)
+
+
+@pytest.mark.parametrize("op", ["sum", "mean"])
+@pytest.mark.parametrize("weighted", [False, True])
+def test_gather_backward_and_sddmm(geot, op, weighted):
+    V, E, S, F = 1_000, 20_000, 800, 32
+    L = synth.segment_lengths(E, S, "powerlaw", 8)
+    dst = synth.lengths_to_index(L, "i64")
+    src = synth.src_index(1008, 0, E, V)
+    x = synth.values(8, 0, V, F, "f32", "int")
+    w = (np.random.default_rng(1).integers(1, 4, size=E).astype(np.float32)) if weighted else None
+    dY = np.random.default_rng(2).integers(-3, 4, size=(S, F)).astype(np.float64)
+    dx_ref, dw_ref = oracle.gather_segment_reduce_backward(dY, x, src, dst, op, weight=w)
+    xt = torch.from_numpy(x).cuda().requires_grad_(True)
+    wt = torch.from_numpy(w).cuda().requires_grad_(True) if weighted else None
+    srct, dstt = torch.from_numpy(src).cuda(), torch.from_numpy(dst).cuda()
+    if weighted and op == "mean":
+        pytest.skip("weighted form is sum-only (P:330)")
+    y = geot.index_segment_reduce_autograd(srct, dstt, xt, op, weight=wt, num_segments=S)
+    y.backward(torch.from_numpy(dY).float().cuda())
+    tol = dict(rtol=1e-5, atol=1e-4) if op == "mean" else dict(rtol=0, atol=0)
+    np.testing.assert_allclose(xt.grad.cpu().numpy(), dx_ref, **tol)  # integer sums: exact for sum
+    if weighted:
+        np.testing.assert_allclose(wt.grad.cpu().numpy(), dw_ref, rtol=1e-6, atol=1e-6)

@@ -167,8 +167,20 @@ def selector_grid():
     return g
 
 
+def selector_grid_large():
+    """Large bf16 / fp32 streams (products-shaped and beyond)."""
+    g = []
+    for F in (64, 128):
+        for E in (1 << 24, 1 << 25, 61_859_140):
+            g.append((E, E // 25, F, "bf16", "powerlaw", "sum", False))
+    for F in (128, 256):
+        g.append((1 << 25, (1 << 25) // 25, F, "f32", "powerlaw", "sum", False))
+    return g
+
+
 GRIDS = {
     "selector": selector_grid(),
+    "selector_large": selector_grid_large(),
     "arxiv": [(ARXIV[0], ARXIV[1], 128, "f32", "powerlaw", "sum", False)],
     "main": [
         (ARXIV[0], ARXIV[1], 128, "f32", "powerlaw", "sum", False),
