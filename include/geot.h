@@ -102,7 +102,9 @@ typedef struct geot_config {
                                STREAM: rows per lane group per ring stage     */
     int32_t warps_per_cta;  /* EDGE_TILE: 8; STREAM: 8 or 16                   */
     int32_t ctas_per_sm;    /* persistent-grid multiplier; 0 = occupancy max   */
-    int32_t stages;         /* STREAM: ring stages per warp (4, 6 or 8)        */
+    int32_t stages;         /* STREAM: TMA ring stages per warp (4, 6, 8), or
+                               1 = no ring: 128-bit LDG into a register double
+                               buffer (2 CTAs per SM); 0 = auto              */
     int32_t reserved;       /* must be 0                                       */
 } geot_config;
 

@@ -121,11 +121,11 @@ static WsLayout ws_layout(long long ntiles, long long F) {
     return w;
 }
 
-long long stream_agents(long long nnz, int lpr, int warps, int nsm) {
+long long stream_agents(long long nnz, int lpr, int warps, int nsm, int ctas_per_sm) {
     if (warps != 8 && warps != 16) return 0;
     const long long per_cta = (long long)warps * (32 / lpr);
     long long grid = nnz / per_cta;
-    if (grid > nsm) grid = nsm;
+    if (grid > (long long)nsm * ctas_per_sm) grid = (long long)nsm * ctas_per_sm;
     return grid >= 1 ? grid * per_cta : 0;
 }
 
@@ -292,7 +292,8 @@ static geot_status reduce_common(const void* X, long long V, const void* src_idx
     }
     if (c.variant == GEOT_VARIANT_STREAM) {
         const int nsm = sm_count();
-        const long long NA = stream_agents(nnz, c.lanes_per_row, c.warps_per_cta, nsm);
+        const long long NA =
+            stream_agents(nnz, c.lanes_per_row, c.warps_per_cta, nsm, c.stages == 1 ? 2 : 1);  // LDG mode: 2 CTAs/SM
         if (NA > 0) {
             const WsLayout L = ws_layout(NA, F);
             if (L.total > 0) {
@@ -332,9 +333,9 @@ static geot_status reduce_common(const void* X, long long V, const void* src_idx
             fx.op = (int)op;
             cudaError_t e = dt == GEOT_F32
                                 ? launch_stream_f32(sp, fx, c.lanes_per_row, c.vecs_per_lane, c.warps_per_cta,
-                                                    c.rows_per_group, c.stages, op == GEOT_MAX, nsm, stream)
+                                                    c.rows_per_group, c.stages == 1 ? 0 : c.stages, op == GEOT_MAX, nsm, stream)
                                 : launch_stream_bf16(sp, fx, c.lanes_per_row, c.vecs_per_lane, c.warps_per_cta,
-                                                     c.rows_per_group, c.stages, op == GEOT_MAX, nsm, stream);
+                                                     c.rows_per_group, c.stages == 1 ? 0 : c.stages, op == GEOT_MAX, nsm, stream);
             if (e == cudaErrorNotSupported) return GEOT_ERR_UNSUPPORTED;
             return from_cuda(e);
         }
@@ -442,7 +443,7 @@ size_t geot_workspace_size(int64_t nnz, int64_t num_segments, int64_t F, geot_re
         geot_config c2 = c;
         select_shape_for_vw(F, dtype, &c2);  // its edge-tile fallback shape
         nt = std::max(nt, ntiles_of(nnz, c2));
-        nt = std::max(nt, stream_agents(nnz, c.lanes_per_row, 16, sm_count()));  // 16 warps: the most agents
+        nt = std::max(nt, stream_agents(nnz, c.lanes_per_row, 16, sm_count(), 2));  // upper bound on agents
     } else if (c.variant == GEOT_VARIANT_NARROW) {
         geot_config c2 = c;
         select_shape_for_vw(F, dtype, &c2);  // its edge-tile fallback shape

@@ -115,7 +115,7 @@ cudaError_t run_edge_tile(const EdgeTileParams& p, int ctas_per_sm, int nsm, cud
 
 // Stream kernel: one persistent CTA per SM (fewer when nnz is small so every
 // agent owns >= 1 row).  Agent count = carry slots.
-long long stream_agents(long long nnz, int lpr, int warps, int nsm);
+long long stream_agents(long long nnz, int lpr, int warps, int nsm, int ctas_per_sm);
 
 template <typename T, int LPR, int VPL, bool ISMAX, int W, int RS, int NS>
 cudaError_t run_stream(const StreamParams& p, const EdgeTileParams& fix, int nsm, cudaStream_t st) {
@@ -124,7 +124,8 @@ cudaError_t run_stream(const StreamParams& p, const EdgeTileParams& fix, int nsm
     auto kern = stream_kernel<T, VW, LPR, VPL, ISMAX, W, RS, NS>;
     const size_t smem = stream_smem_bytes(W, NS, G, RS, p.row_bytes);
     if (smem > 227 * 1024) return cudaErrorNotSupported;
-    if (cached_occupancy(kern, W * 32, smem) <= 0) return cudaErrorInvalidConfiguration;
+    const int occ = cached_occupancy(kern, W * 32, smem);
+    if (occ < (NS > 0 ? 1 : 2)) return cudaErrorInvalidConfiguration;  // agents assume this many CTAs/SM
     const long long grid = p.NA / ((long long)W * G);
     if (grid < 1 || grid * W * G != p.NA) return cudaErrorInvalidValue;
     if (g_prof_before) cudaEventRecord(g_prof_before, st);
@@ -151,16 +152,21 @@ cudaError_t launch_stream(const StreamParams& p, const EdgeTileParams& fix, int 
     GEOT_SSHAPE(LPR_, 1, 16, 6, 4)   \
     GEOT_SSHAPE(LPR_, 1, 8, 6, 8)    \
     GEOT_SSHAPE(LPR_, 1, 16, 3, 8)   \
-    GEOT_SSHAPE(LPR_, 1, 8, 8, 6)
+    GEOT_SSHAPE(LPR_, 1, 8, 8, 6)    \
+    GEOT_SSHAPE(LPR_, 1, 8, 4, 0)    \
+    GEOT_SSHAPE(LPR_, 1, 8, 8, 0)
     GEOT_SSHAPE_V1(8)
     GEOT_SSHAPE_V1(16)
     GEOT_SSHAPE_V1(32)
     GEOT_SSHAPE(32, 2, 16, 3, 4)
     GEOT_SSHAPE(32, 2, 8, 3, 8)
+    GEOT_SSHAPE(32, 2, 8, 4, 0)
     GEOT_SSHAPE(32, 4, 8, 3, 4)
+    GEOT_SSHAPE(32, 4, 8, 2, 0)
     if constexpr (sizeof(T) == 4) {
         GEOT_SSHAPE(32, 8, 8, 1, 4)
         GEOT_SSHAPE(32, 8, 8, 1, 6)
+        GEOT_SSHAPE(32, 8, 8, 1, 0)
     }
 #undef GEOT_SSHAPE_V1
 #undef GEOT_SSHAPE

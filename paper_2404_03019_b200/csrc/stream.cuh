@@ -67,8 +67,13 @@ __host__ __device__ inline size_t stream_smem_bytes(int W, int NS, int G, int RS
            + (size_t)W * NS * 8;                     // mbarriers
 }
 
+// NS > 0: TMA bulk-copy ring of NS stages per warp (one CTA per SM).
+// NS == 0: the same agents and carries, rows streamed with 128-bit LDG into a
+//          register double buffer (several CTAs per SM, no shared ring).
 template <typename T, int VW, int LPR, int VPL, bool ISMAX, int W, int RS, int NS>
-__global__ void __launch_bounds__(W * 32, 1) stream_kernel(const StreamParams p) {
+__global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const StreamParams p) {
+    constexpr bool TMA = NS > 0;
+    constexpr int NSX = TMA ? NS : 1;
     constexpr int G = 32 / LPR;
     using Cv = Conv<T, VW>;
     using Raw = typename Cv::Raw;
@@ -120,18 +125,20 @@ __global__ void __launch_bounds__(W * 32, 1) stream_kernel(const StreamParams p)
         ghi[g] = __shfl_sync(0xffffffffu, e_hi, g * LPR);
     }
 
-    // int32 keys land in the low half of 8-byte slots: zero the ring once
-    for (int i = lane; i < NS * G * RS; i += 32) wkey[i] = 0ull;
-    if (lane == 0) {
-        for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1 + 32);  // producer + 32 cp.async arrivals
-        fence_mbar_init();
+    if constexpr (TMA) {
+        // int32 keys land in the low half of 8-byte slots: zero the ring once
+        for (int i = lane; i < NS * G * RS; i += 32) wkey[i] = 0ull;
+        if (lane == 0) {
+            for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1 + 32);  // producer + 32 cp.async arrivals
+            fence_mbar_init();
+        }
+        __syncwarp();
     }
-    __syncwarp();
     const uint64_t pol = policy_evict_first();
 
     // all lanes: fill stage s of every group of the warp into buffer s % NS
     auto issue = [&](int s) {
-        const int b = s % NS;
+        const int b = s % NSX;
         if (lane == 0) {
             unsigned char* buf = wbuf + b * stage_bytes;
             uint32_t total = 0;
@@ -160,7 +167,8 @@ __global__ void __launch_bounds__(W * 32, 1) stream_kernel(const StreamParams p)
         }
         cp_async_mbar_arrive(&bars[b]);
     };
-    for (int s = 0; s < NS && s < nst_w; ++s) issue(s);
+    if constexpr (TMA)
+        for (int s = 0; s < NS && s < nst_w; ++s) issue(s);
 
     const long long prevk = (e_lo > 0) ? load_index(p.idx, p.idx64, e_lo - 1) : KEY_BEFORE;
     const long long nextk = (e_hi < p.E) ? load_index(p.idx, p.idx64, e_hi) : KEY_AFTER;
@@ -224,36 +232,17 @@ __global__ void __launch_bounds__(W * 32, 1) stream_kernel(const StreamParams p)
     bool col_ok[VPL];
 #pragma unroll
     for (int j = 0; j < VPL; ++j) col_ok[j] = vec_col(j) < p.NV;
-    // 32-bit shared address of this lane's first vector in group gi's rows of buffer 0
-    const uint32_t lane_s0 = smem_u32(wbuf) + gi * RS * row_bytes + li * 16;
-
-#pragma unroll 1
-    for (int s = 0; s < nst_w; ++s) {
-        const int b = s % NS;
-        mbar_wait(&bars[b], (uint32_t)((s / NS) & 1));
-        const uint32_t sbase = lane_s0 + b * stage_bytes;
-        const long long* gkey = reinterpret_cast<const long long*>(wkey + (b * G + gi) * RS);
-        const long long r_base = e_lo + (long long)s * RS;
-        int cnt = (int)(e_hi - r_base);
-        cnt = cnt < 0 ? 0 : (cnt > RS ? RS : cnt);
-        // the whole stage's rows into registers at once (RS x VPL x 16 B per lane)
-        Raw rows[RS][VPL];
-#pragma unroll
-        for (int r = 0; r < RS; ++r)
-#pragma unroll
-            for (int j = 0; j < VPL; ++j)
-                rows[r][j] = (r < cnt && col_ok[j]) ? lds_vec<Raw>(sbase + r * row_bytes + j * LPR * 16) : Raw{};
+    // one stage of RS rows (already in registers) + this lane's key (row li)
+    auto process = [&](const Raw (&rows)[RS][VPL], long long kmine, long long kprev, int cnt, long long r_base) {
         // is_seg of the whole stage (Alg. 1): row r starts a segment iff its
         // key differs from row r-1's (row -1: `cur`)
-        const long long kmine = (li < cnt) ? gkey[li] : KEY_AFTER;
-        const long long kprev = (li == 0) ? cur : ((li <= cnt) ? gkey[li - 1] : KEY_AFTER);
         const unsigned heads = __ballot_sync(gmask, li < cnt && kmine != kprev) >> (gi * LPR);
 #pragma unroll
         for (int r = 0; r < RS; ++r) {
             if (r >= cnt) break;
             const Raw (&raw)[VPL] = rows[r];
             if ((heads >> r) & 1u) {  // segment `cur` ended at the previous row
-                const long long k = gkey[r];
+                const long long k = __shfl_sync(gmask, kmine, r, LPR);
                 const long long e = r_base + r;
                 if (first && head_open) {
 #pragma unroll
@@ -282,8 +271,73 @@ __global__ void __launch_bounds__(W * 32, 1) stream_kernel(const StreamParams p)
                 for (int q = 0; q < VW; ++q) acc[j][q] = fold<ISMAX>(acc[j][q], f[q]);
             }
         }
-        __syncwarp();
-        if (s + NS < nst_w) issue(s + NS);
+    };
+
+    if constexpr (TMA) {
+        // 32-bit shared address of this lane's first vector in group gi's rows of buffer 0
+        const uint32_t lane_s0 = smem_u32(wbuf) + gi * RS * row_bytes + li * 16;
+#pragma unroll 1
+        for (int s = 0; s < nst_w; ++s) {
+            const int b = s % NSX;
+            mbar_wait(&bars[b], (uint32_t)((s / NSX) & 1));
+            const uint32_t sbase = lane_s0 + b * stage_bytes;
+            const long long* gkey = reinterpret_cast<const long long*>(wkey + (b * G + gi) * RS);
+            const long long r_base = e_lo + (long long)s * RS;
+            int cnt = (int)(e_hi - r_base);
+            cnt = cnt < 0 ? 0 : (cnt > RS ? RS : cnt);
+            // the whole stage's rows into registers at once (RS x VPL x 16 B per lane)
+            Raw rows[RS][VPL];
+#pragma unroll
+            for (int r = 0; r < RS; ++r)
+#pragma unroll
+                for (int j = 0; j < VPL; ++j)
+                    rows[r][j] = (r < cnt && col_ok[j]) ? lds_vec<Raw>(sbase + r * row_bytes + j * LPR * 16) : Raw{};
+            const long long kmine = (li < cnt) ? gkey[li] : KEY_AFTER;
+            const long long kprev = (li == 0) ? cur : ((li <= cnt) ? gkey[li - 1] : KEY_AFTER);
+            // the stage now lives in registers: hand its buffer back to the TMA
+            // producer right away (the proxy fence orders these shared-memory
+            // reads before the async-proxy writes of the refill)
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (s + NSX < nst_w) issue(s + NSX);
+            process(rows, kmine, kprev, cnt, r_base);
+        }
+    } else {
+        // LDG path: the next stage's rows and key are loaded into registers
+        // (128-bit ld.global.nc.L1::no_allocate) while the current one is reduced
+        Raw nxt[RS][VPL];
+        long long nkey = KEY_AFTER;
+        auto fetch = [&](int s) {
+            const long long rb = e_lo + (long long)s * RS;
+            int c = (int)(e_hi - rb);
+            c = c < 0 ? 0 : (c > RS ? RS : c);
+            const T* base = X + rb * (long long)F;
+#pragma unroll
+            for (int r = 0; r < RS; ++r)
+#pragma unroll
+                for (int j = 0; j < VPL; ++j)
+                    nxt[r][j] = (r < c && col_ok[j])
+                                    ? ld_stream(reinterpret_cast<const Raw*>(base + (long long)r * F + vec_col(j) * VW))
+                                    : Raw{};
+            nkey = (li < c) ? load_index(p.idx, p.idx64, rb + li) : KEY_AFTER;
+        };
+        if (nst > 0) fetch(0);
+#pragma unroll 1
+        for (int s = 0; s < nst; ++s) {
+            Raw rows[RS][VPL];
+#pragma unroll
+            for (int r = 0; r < RS; ++r)
+#pragma unroll
+                for (int j = 0; j < VPL; ++j) rows[r][j] = nxt[r][j];
+            const long long kmine = nkey;
+            if (s + 1 < nst) fetch(s + 1);
+            const long long r_base = e_lo + (long long)s * RS;
+            int cnt = (int)(e_hi - r_base);
+            cnt = cnt > RS ? RS : cnt;
+            long long kprev = __shfl_up_sync(gmask, kmine, 1, LPR);
+            if (li == 0) kprev = cur;
+            process(rows, kmine, kprev, cnt, r_base);
+        }
     }
 
     // ---- agent end: publish the carries later agents need (H5) ...

@@ -68,8 +68,9 @@ def make_inputs(E, S, F, dtype, dist, seed, fused=False, V=None, itype=torch.int
     return L, idx, X, None
 
 
-STREAM_PIPES = {1: [(16, 6, 4), (8, 6, 8), (16, 3, 8), (8, 8, 6)], 2: [(16, 3, 4), (8, 3, 8)], 4: [(8, 3, 4)],
-                8: [(8, 1, 4), (8, 1, 6)]}
+STREAM_PIPES = {1: [(16, 6, 4), (8, 6, 8), (16, 3, 8), (8, 8, 6), (8, 4, 1), (8, 8, 1)],
+                2: [(16, 3, 4), (8, 3, 8), (8, 4, 1)], 4: [(8, 3, 4), (8, 2, 1)],
+                8: [(8, 1, 4), (8, 1, 6), (8, 1, 1)]}
 
 
 def candidate_configs(E, S, F, dtype, fused, quick=False):
