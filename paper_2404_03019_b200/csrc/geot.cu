@@ -265,7 +265,8 @@ static geot_status reduce_common(const void* X, long long V, const void* src_idx
     }
     unsigned char* wsb = static_cast<unsigned char*>(ws);
     if (c.variant == GEOT_VARIANT_NARROW) {
-        if (mode == 0 && aligned(X, 16) && aligned(idx, 16)) {
+        if (mode == 0 && aligned(X, 16) && aligned(idx, 16) &&
+            (it == GEOT_I64 || seg_base + S < (long long)INT_MAX)) {  // 32-bit key arithmetic
             const int nsm = sm_count();
             const WsLayout L = ws_layout(narrow_agents_max(nsm), F);
             if (!ws) return GEOT_ERR_INVALID_VALUE;

@@ -12,7 +12,7 @@ import synth.device as sd  # noqa: E402
 
 E, S, F = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3])
 dt, dist = sys.argv[4], sys.argv[5]
-cfg = json.loads(sys.argv[6]) if len(sys.argv) > 6 and sys.argv[6] else None
+cfg = json.loads(sys.argv[6]) if len(sys.argv) > 6 and sys.argv[6] not in ("", "-") else None
 fused = len(sys.argv) > 7 and sys.argv[7] == "fused"
 tdt = torch.float32 if dt == "f32" else torch.bfloat16
 L = synth.segment_lengths(E, S, dist, 5)
