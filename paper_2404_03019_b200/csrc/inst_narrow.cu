@@ -1,14 +1,57 @@
-// Instantiations + launcher of the small-F kernel family (narrow.cuh).
+// Instantiations + launcher of the small-F kernel family (narrow.cuh): the
+// two 2-D TMA tensor maps (values / keys viewed as rows of one lane's chunk
+// bytes, swizzled to the lane-row width) are encoded here, per call.
+#include <cuda.h>
+
+#include <mutex>
+
 #include "launch.cuh"
 #include "narrow.cuh"
 
 namespace geot {
 
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(f);
+    });
+    return fn;
+}
+
+// rows of LB bytes over [base, base + nrows*LB), box = 32 rows, swizzle = LB
+static bool encode_rows(CUtensorMap* m, const void* base, long long nrows, int lb) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn || nrows < 32 || nrows > 0x7fffffffLL) return false;
+    const cuuint64_t dims[2] = {(cuuint64_t)lb, (cuuint64_t)nrows};
+    const cuuint64_t strides[1] = {(cuuint64_t)lb};
+    const cuuint32_t box[2] = {(cuuint32_t)lb, 32u};
+    const cuuint32_t estr[2] = {1u, 1u};
+    const CUtensorMapSwizzle sw = lb == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
+                                  : lb == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                  : lb == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                             : CU_TENSOR_MAP_SWIZZLE_NONE;
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <typename T, int F, int OP, bool I64>
 static cudaError_t run_narrow(NarrowParams p, int nsm, cudaStream_t st) {
-    constexpr int ITEMS = narrow_items(F, (int)sizeof(T), I64 ? 8 : 4);
+    constexpr int KSZ = I64 ? 8 : 4;
+    constexpr int ITEMS = narrow_items(F, (int)sizeof(T), KSZ);
+    constexpr int LBV = ITEMS * F * (int)sizeof(T), LBK = ITEMS * KSZ;
     auto kern = narrow_kernel<T, F, ITEMS, OP, I64>;
-    int occ = cached_occupancy(kern, kNarrowWarps * 32, 0);
+    const size_t smem = narrow_smem_bytes(LBV, LBK);
+    int occ = cached_occupancy(kern, kNarrowWarps * 32, smem);
     if (occ <= 0) return cudaErrorInvalidConfiguration;
     // every agent (warp) must own at least one chunk of 32*ITEMS rows
     long long grid = (long long)nsm * occ;
@@ -16,8 +59,14 @@ static cudaError_t run_narrow(NarrowParams p, int nsm, cudaStream_t st) {
     if (grid * kNarrowWarps > max_agents) grid = max_agents / kNarrowWarps;
     if (grid < 1) return cudaErrorNotSupported;
     p.NA = grid * kNarrowWarps;
+    // whole lane rows only: the tail (< one lane row) is read directly
+    CUtensorMap tmv, tmk;
+    memset(&tmv, 0, sizeof(tmv));
+    memset(&tmk, 0, sizeof(tmk));
+    const long long nrows = p.E / ITEMS;
+    p.tma = (LBV >= 16 && LBK >= 16 && encode_rows(&tmv, p.X, nrows, LBV) && encode_rows(&tmk, p.idx, nrows, LBK)) ? 1 : 0;
     if (g_prof_before) cudaEventRecord(g_prof_before, st);
-    kern<<<(unsigned)grid, kNarrowWarps * 32, 0, st>>>(p);
+    kern<<<(unsigned)grid, kNarrowWarps * 32, smem, st>>>(tmv, tmk, p);
     if (g_prof_after) cudaEventRecord(g_prof_after, st);
     g_prof_before = g_prof_after = nullptr;
     cudaError_t e = cudaGetLastError();

@@ -9,9 +9,11 @@
 //    (balanced), one persistent grid, in-kernel carry resolution exactly as in
 //    stream.cuh (ticketed CTAs, epoch-published agent carries);
 //  * a warp processes chunks of 32*ITEMS rows; lane l owns ITEMS consecutive
-//    rows (64 bytes of values), fetched with 128-bit loads of values and keys
-//    one chunk ahead (register double buffer; the lane-contiguous 16-byte
-//    pieces of one sector are merged in L1, so DRAM sees every byte once);
+//    rows.  A chunk's values and keys are two 2-D TMA tensor tiles (32 lane
+//    rows of LB bytes each) landing in a per-warp NS-stage shared-memory ring
+//    with the 32/64/128-byte swizzle, so that every lane reading its own LB
+//    contiguous bytes with 128-bit LDS is bank-conflict free.  One elected lane
+//    issues two TMA copies per chunk; nothing is double-buffered in registers;
 //  * lane pass (SR within the lane): is_seg of every item (Alg. 1:
 //    key != previous key) as one bit mask, then a predicated sequential
 //    accumulation that restarts at heads.  Every segment that STARTS and ENDS
@@ -23,11 +25,14 @@
 //    carry of the segment that continues into it from the left, which the lane
 //    folds into that segment's in-lane prefix (read back from a per-warp
 //    shared-memory copy of the lane's partials: one dynamic index, no select
-//    chain) and stores once where it ends;
+//    chain) and stores once where it ends.  A segment ending exactly at a
+//    chunk boundary is stored by the next chunk's lane 0 (no look-ahead load);
 //  * empty segments: a lane whose key span (last key - key before its first
 //    row) differs from its number of segment heads has a gap (or unsorted
-//    data) and zero-fills it item by item (rare path).
+//    data) and zero-fills it (rare path, keys re-read from the ring).
 #pragma once
+
+#include <cuda.h>
 
 #include "common.cuh"
 #include "stream.cuh"
@@ -46,40 +51,66 @@ struct NarrowParams {
     long long E, seg_base, S;
     long long NA;  // agents = warps of the grid
     int op;
+    int tma;       // 1: full chunks come through the TMA ring (tensor maps valid)
 };
 
 constexpr int kNarrowWarps = 8;
 
-// rows per lane per chunk: at most 64 value bytes, 128 value + key bytes and
-// 16 rows per lane (register budget of the double buffer)
+// rows per lane per chunk: at most 128 value bytes, 64 key bytes, 32 fp32
+// partials and 16 rows per lane (power of two)
 __host__ __device__ constexpr int narrow_items(int F, int esz, int ksz) {
-    int r = 64 / (F * esz) < 16 ? 64 / (F * esz) : 16;
-    while (r > 2 && r * (F * esz + ksz) > 128) r /= 2;
+    int r = 16;
+    while (r > 2 && (r * F * esz > 128 || r * ksz > 64 || r * F > 32)) r /= 2;
     return r;
 }
+// one ring area (values or keys tile of 32 lane rows), 1024-byte aligned (swizzle atom)
+__host__ __device__ constexpr int narrow_area(int lb) { return ((32 * lb + 1023) / 1024) * 1024; }
+__host__ __device__ constexpr int narrow_stage_bytes(int lbv, int lbk) { return narrow_area(lbv) + narrow_area(lbk); }
+// ring depth: 3 stages of <= 4 KB, else 2 (two 8-warp CTAs per SM fit either way)
+__host__ __device__ constexpr int narrow_stages(int lbv, int lbk) { return narrow_stage_bytes(lbv, lbk) <= 4096 ? 3 : 2; }
+__host__ __device__ constexpr size_t narrow_smem_bytes(int lbv, int lbk) {
+    return (size_t)kNarrowWarps * narrow_stages(lbv, lbk) * narrow_stage_bytes(lbv, lbk)  // rings
+           + (size_t)kNarrowWarps * narrow_stages(lbv, lbk) * 8                          // mbarriers
+           + 1024;                                                                       // alignment slack
+}
 
-// raw 32-bit words of NB bytes at p (NB multiple of 8; 16-byte pieces when
-// possible).  L1-allocating loads: the lanes' 16-byte pieces of one sector
-// arrive in separate instructions and are merged in L1.
-template <int NB>
-__device__ __forceinline__ void ld_words(const void* p, uint32_t (&w)[NB / 4]) {
-    static_assert(NB % 8 == 0, "8-byte granularity");
-    if constexpr (NB % 16 == 0) {
+// physical offset of logical byte o of a tile written by TMA with the swizzle
+// matching a lane row of LB bytes (16B chunk bits [4,4+b) ^= bits [7,7+b))
+template <int LB>
+__device__ __forceinline__ uint32_t swz(uint32_t o) {
+    if constexpr (LB == 32) return o ^ (((o >> 7) & 1u) << 4);
+    if constexpr (LB == 64) return o ^ (((o >> 7) & 3u) << 4);
+    if constexpr (LB == 128) return o ^ (((o >> 7) & 7u) << 4);
+    return o;
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
+                                            uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+
+// 32-bit words of LB bytes of a lane row from the (swizzled) ring
+template <int LB>
+__device__ __forceinline__ void lds_row(uint32_t base, int lane, uint32_t (&w)[LB / 4]) {
+    static_assert(LB % 8 == 0, "8-byte granularity");
+    if constexpr (LB % 16 == 0) {
 #pragma unroll
-        for (int i = 0; i < NB / 16; ++i) {
-            const uint4 v = ld_cached(reinterpret_cast<const uint4*>(p) + i);
-            w[4 * i] = v.x;
-            w[4 * i + 1] = v.y;
-            w[4 * i + 2] = v.z;
-            w[4 * i + 3] = v.w;
+        for (int q = 0; q < LB / 16; ++q) {
+            const uint4 v = lds_vec<uint4>(base + swz<LB>((uint32_t)(lane * LB + q * 16)));
+            w[4 * q] = v.x;
+            w[4 * q + 1] = v.y;
+            w[4 * q + 2] = v.z;
+            w[4 * q + 3] = v.w;
         }
-    } else {
-#pragma unroll
-        for (int i = 0; i < NB / 8; ++i) {
-            const uint2 v = __ldg(reinterpret_cast<const uint2*>(p) + i);
-            w[2 * i] = v.x;
-            w[2 * i + 1] = v.y;
-        }
+    } else {  // LB == 8 (two int32 keys): unswizzled 8-byte rows
+        uint32_t x, y;
+        asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(x), "=r"(y) : "r"(base + lane * 8));
+        w[0] = x;
+        w[1] = y;
     }
 }
 
@@ -142,25 +173,28 @@ __device__ __forceinline__ float nident() {
     return identity<OP == OP_MAX>();
 }
 
-// Rows per CTA for the occupancy target: the register double buffer holds
-// 2 x 64 value bytes + 2 x ITEMS keys per lane.
 template <typename T, int F, int ITEMS, int OP, bool I64>
-__global__ void __launch_bounds__(kNarrowWarps * 32, 2) narrow_kernel(const NarrowParams p) {
-    constexpr int CH = 32 * ITEMS;             // rows per chunk
+__global__ void __launch_bounds__(kNarrowWarps * 32, 2)
+    narrow_kernel(const __grid_constant__ CUtensorMap tmv, const __grid_constant__ CUtensorMap tmk,
+                  const NarrowParams p) {
+    constexpr int CH = 32 * ITEMS;        // rows per chunk
     constexpr int ESZ = sizeof(T);
-    constexpr int VB = ITEMS * F * ESZ;        // value bytes per lane per chunk
-    constexpr int KB = ITEMS * (I64 ? 8 : 4);  // key bytes per lane per chunk
-    constexpr int VWORDS = VB / 4, KWORDS = KB / 4;
-    constexpr int NACC = ITEMS * F;            // fp32 partials per lane
-    static_assert(NACC % 4 == 0 || NACC < 4, "partials are spilled in 16-byte pieces");
-    constexpr int NQ = (NACC + 3) / 4;         // 16-byte pieces of partials per lane
+    constexpr int KSZ = I64 ? 8 : 4;
+    constexpr int LBV = ITEMS * F * ESZ;  // value bytes per lane per chunk
+    constexpr int LBK = ITEMS * KSZ;      // key bytes per lane per chunk
+    constexpr int VWORDS = LBV / 4, KWORDS = LBK / 4;
+    constexpr int NS = narrow_stages(LBV, LBK);
+    constexpr int AREA_V = narrow_area(LBV);
+    constexpr int STAGE = narrow_stage_bytes(LBV, LBK);
     using KT = typename std::conditional<I64, long long, int>::type;
-    constexpr bool ISMAX = OP == OP_MAX;
 
-    // per-warp copy of every lane's partials, piece-major [q][lane] (conflict-free)
-    __shared__ float4 s_acc[kNarrowWarps][NQ][32];
-
+    extern __shared__ __align__(16) unsigned char smem_dyn[];
+    // the swizzle pattern is a function of the shared address: 1024-byte align the rings
+    unsigned char* smem_raw = smem_dyn + ((1024u - (smem_u32(smem_dyn) & 1023u)) & 1023u);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t ring = smem_u32(smem_raw) + (uint32_t)(warp * NS * STAGE);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + (size_t)kNarrowWarps * NS * STAGE) + warp * NS;
+
     const T* __restrict__ X = static_cast<const T*>(p.X);
     const KT* __restrict__ I = static_cast<const KT*>(p.idx);
     T* __restrict__ out = static_cast<T*>(p.out);
@@ -182,6 +216,26 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, 2) narrow_kernel(const Narr
         return ((x * E) / p.NA) / ITEMS * ITEMS;
     };
     const long long e_lo = agent_lo(a), e_hi = agent_lo(a + 1);
+    const int nchunks = (int)((e_hi - e_lo + CH - 1) / CH);
+    // every chunk comes through the TMA ring (rows past the tensor are zero-filled
+    // by TMA; the global tail lane row, if partial, is read directly)
+    const int nring = p.tma ? nchunks : 0;
+
+    const uint64_t pol = policy_evict_first();
+    if (lane == 0) {
+        for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    auto issue = [&](int s) {  // lane 0: chunk s into stage s % NS
+        const int b = s % NS;
+        const int row = (int)((e_lo + (long long)s * CH) / ITEMS);  // lane-row coordinate
+        mbar_arrive_expect_tx(&bars[b], 32u * (LBV + LBK));
+        tma_load_2d(ring + b * STAGE, &tmv, 0, row, &bars[b], pol);
+        tma_load_2d(ring + b * STAGE + AREA_V, &tmk, 0, row, &bars[b], pol);
+    };
+    if (lane == 0)
+        for (int s = 0; s < NS && s < nring; ++s) issue(s);
 
     auto key_at = [&](long long e) -> long long { return (long long)__ldg(I + e); };
     // zero rows strictly between keys lo_k and hi_k, clamped to [seg_lo, seg_hi)
@@ -196,18 +250,21 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, 2) narrow_kernel(const Narr
     // a store at key k (32-bit relative arithmetic for int32 keys; memory-safe)
     const KT kseg_lo = (KT)seg_lo;
     const unsigned long long nseg = (unsigned long long)p.S;
-    auto store_at = [&](KT k, const float (&v)[F], int count) {
+    auto store_at = [&](bool pred, KT k, const float (&v)[F], int count) {
+        bool ok;
         unsigned long long rel;
-        if constexpr (I64)
+        if constexpr (I64) {
             rel = (unsigned long long)(k - kseg_lo);
-        else
-            rel = (unsigned long long)((unsigned)k - (unsigned)kseg_lo);  // wraps for keys < seg_lo
-        if (rel < nseg) {
-            float o[F];
-#pragma unroll
-            for (int f = 0; f < F; ++f) o[f] = (OP == OP_MEAN) ? __fdiv_rn(v[f], (float)count) : v[f];
-            st_row<T, F>(out + rel * F, o);
+            ok = pred && rel < nseg;
+        } else {
+            const unsigned r32 = (unsigned)k - (unsigned)kseg_lo;  // wraps for keys < seg_lo
+            ok = pred && r32 < (unsigned)nseg;                      // S < 2^31 on this path
+            rel = r32;
         }
+        float o[F];
+#pragma unroll
+        for (int f = 0; f < F; ++f) o[f] = (OP == OP_MEAN) ? __fdiv_rn(v[f], (float)count) : v[f];
+        if (ok) st_row<T, F>(out + rel * F, o);
     };
 
     const bool active = e_lo < e_hi;
@@ -224,38 +281,31 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, 2) narrow_kernel(const Narr
     float rc[F];  // value of the open segment (from its start, or from e_lo for the head segment)
 #pragma unroll
     for (int f = 0; f < F; ++f) rc[f] = nident<OP>();
-    KT rkey = kprev0;     // key of the last row before the current chunk
-    long long rpos = 0;   // start row (relative to e_lo) of the open segment (mean counts)
+    KT rkey = kprev0;        // key of the last row before the current chunk
+    long long rpos = 0;      // start row (relative to e_lo) of the open segment (mean counts)
     bool rhead = head_open;  // the open segment began in an earlier agent
-    float hacc[F];        // this agent's partial of that head segment, once it ends here
+    float hacc[F];           // this agent's partial of that head segment, once it ends here
 #pragma unroll
     for (int f = 0; f < F; ++f) hacc[f] = nident<OP>();
     long long head_end = -1;
 
-    uint32_t nvw[VWORDS], nkw[KWORDS];  // next chunk (full lanes only)
-    auto prefetch = [&](long long c) {
-        const long long r = c + (long long)lane * ITEMS;
-        if (r + ITEMS <= e_hi) {
-            ld_words<VB>(X + r * F, nvw);
-            ld_words<KB>(I + r, nkw);
-        }
-    };
-    prefetch(e_lo);
 #pragma unroll 1
-    for (long long c0 = e_lo; c0 < e_hi; c0 += CH) {
+    for (int s = 0; s < nchunks; ++s) {
+        const long long c0 = e_lo + (long long)s * CH;
         const long long r0 = c0 + (long long)lane * ITEMS;  // this lane's first row
-        long long nvl = e_hi - r0;
-        const int nv = nvl <= 0 ? 0 : (nvl >= ITEMS ? ITEMS : (int)nvl);  // valid items
-        const bool full_chunk = c0 + CH <= e_hi;                           // warp-uniform
+        const bool last_chunk = s == nchunks - 1;  // warp-uniform
+        const long long nvl = e_hi - r0;
+        const int nv = nvl <= 0 ? 0 : (nvl >= ITEMS ? ITEMS : (int)nvl);  // valid items of the lane
+        // a lane whose row is not in the ring: the global tail row, or no tensor maps
+        const bool direct = !p.tma || (nv > 0 && r0 + ITEMS > E);
         float acc[ITEMS][F];
         KT k[ITEMS];
-        if (nv == ITEMS) {
+        const int b = s % NS;
+        if (p.tma) {
+            mbar_wait(&bars[b], (uint32_t)((s / NS) & 1));
             uint32_t vw[VWORDS], kw[KWORDS];
-#pragma unroll
-            for (int i = 0; i < VWORDS; ++i) vw[i] = nvw[i];
-#pragma unroll
-            for (int i = 0; i < KWORDS; ++i) kw[i] = nkw[i];
-            prefetch(c0 + CH);
+            lds_row<LBV>(ring + b * STAGE, lane, vw);
+            lds_row<LBK>(ring + b * STAGE + AREA_V, lane, kw);
 #pragma unroll
             for (int i = 0; i < ITEMS; ++i) {
 #pragma unroll
@@ -265,33 +315,37 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, 2) narrow_kernel(const Narr
                 else
                     k[i] = (int)kw[i];
             }
-        } else {  // the agent's last chunk: partial lanes
+        }
+        if (__any_sync(0xffffffffu, direct)) {
+            if (direct) {
+#pragma unroll
+                for (int i = 0; i < ITEMS; ++i) {
+                    const bool ok = i < nv;
+#pragma unroll
+                    for (int f = 0; f < F; ++f) acc[i][f] = ok ? ld_elem<T>(X + (r0 + i) * F + f) : 0.f;
+                    k[i] = ok ? __ldg(I + r0 + i) : (KT)0;
+                }
+            }
+        }
+        if (last_chunk) {  // lanes past the agent's end: padding never starts a segment
+            if (nv == 0) k[0] = 0;
 #pragma unroll
             for (int i = 0; i < ITEMS; ++i) {
-                const bool ok = i < nv;
+                if (i >= nv) {
+                    if (i > 0) k[i] = k[i - 1];
 #pragma unroll
-                for (int f = 0; f < F; ++f) acc[i][f] = ok ? ld_elem<T>(X + (r0 + i) * F + f) : nident<OP>();
-                k[i] = ok ? __ldg(I + r0 + i) : (KT)0;
+                    for (int f = 0; f < F; ++f) acc[i][f] = nident<OP>();
+                }
             }
-#pragma unroll
-            for (int i = 1; i < ITEMS; ++i)
-                if (i >= nv) k[i] = k[i - 1];  // padding never starts a segment
         }
         // neighbours: the key before the lane's first row and after its last row
+        // (lane 31 of a chunk that is not the agent's last: unknown -> "continues";
+        // a segment ending there is stored by the next chunk's lane 0)
         KT kp = __shfl_up_sync(0xffffffffu, k[ITEMS - 1], 1);
         if (lane == 0) kp = rkey;
         KT kn = __shfl_down_sync(0xffffffffu, k[0], 1);
-        {
-            // lane 31 of a full chunk: the next chunk's first key (lane 0's prefetch)
-            KT pf;
-            if constexpr (I64)
-                pf = (long long)(((unsigned long long)nkw[1] << 32) | nkw[0]);
-            else
-                pf = (int)nkw[0];
-            pf = __shfl_sync(0xffffffffu, pf, 0);
-            if (lane == 31 && full_chunk) kn = (c0 + CH + ITEMS <= e_hi) ? pf : (KT)((c0 + CH < e_hi) ? key_at(c0 + CH) : (long long)knext_end);
-            if (nv > 0 && r0 + nv >= e_hi) kn = knext_end;  // the agent's last row
-        }
+        if (lane == 31) kn = k[ITEMS - 1];
+        if (last_chunk && nv > 0 && r0 + nv >= e_hi) kn = knext_end;  // the agent's last row
 
         // ---- lane pass: heads (is_seg), sequential accumulation with restarts
         unsigned hm = (nv > 0 && k[0] != kp) ? 1u : 0u;
@@ -306,27 +360,66 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, 2) narrow_kernel(const Narr
         const KT klast = k[ITEMS - 1];  // padded: the last valid key
         const bool last_ends = nv > 0 && klast != kn;
         const unsigned em = (hm >> 1) | ((unsigned)last_ends << (nv > 0 ? nv - 1 : 0));  // items ending a segment
-
         // segments that start and end inside the lane: store now
+        const unsigned smk = em & ~((hm & (0u - hm)) - 1u);
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
-            const unsigned upto = (2u << i) - 1u;
-            if (((em >> i) & 1u) && (hm & upto)) {
-                int cnt = 1;
-                if constexpr (OP == OP_MEAN) cnt = i + 1 - (31 - __clz(hm & upto));
-                store_at(k[i], acc[i], cnt);
+            int cnt = 1;
+            if constexpr (OP == OP_MEAN) cnt = i + 1 - (31 - __clz(hm & ((2u << i) - 1u)));
+            store_at((smk >> i) & 1u, k[i], acc[i], cnt);  // predicated, no branch
+        }
+        // the running segment ended exactly at the previous chunk's end
+        if (lane == 0 && s > 0 && (hm & 1u)) {
+            if (rhead) {
+#pragma unroll
+                for (int f = 0; f < F; ++f) hacc[f] = rc[f];
+                head_end = c0;
+            } else {
+                store_at(true, rkey, rc, (int)((c0 - e_lo) - rpos));
             }
         }
 
-        // gaps (empty segments) or unsorted keys: key span != number of heads
-        if (nv > 0 && (long long)klast - (long long)kp != (long long)__popc(hm)) {
-            long long pk = (long long)kp;
-#pragma unroll
-            for (int i = 0; i < ITEMS; ++i)
-                if ((hm >> i) & 1u) {
-                    if ((long long)k[i] != pk + 1) gap_fill(pk, (long long)k[i]);
-                    pk = (long long)k[i];
+        // gaps (empty segments) or unsorted keys: a lane whose key span differs
+        // from its number of heads.  Rare per lane, but some lane of most chunks
+        // has one: the warp takes those lanes one at a time, lane i examining item
+        // i of the gap lane (keys from the ring) and zero-filling its gap
+        {
+            const bool gap = nv > 0 && (long long)klast - (long long)kp != (long long)__popc(hm);
+            unsigned gl = __ballot_sync(0xffffffffu, gap);
+            while (gl) {
+                const int g = __ffs(gl) - 1;
+                gl &= gl - 1;
+                const KT gkp = __shfl_sync(0xffffffffu, kp, g);
+                const int gnv = __shfl_sync(0xffffffffu, nv, g);
+                const bool gdirect = __shfl_sync(0xffffffffu, (int)direct, g) != 0;
+                const long long gr0 = c0 + (long long)g * ITEMS;
+                long long kc = 0, kq = 0;  // key of item `lane` of lane g and of the item before it
+                if (lane < gnv) {
+                    if (!gdirect) {
+                        const uint32_t kb = ring + b * STAGE + AREA_V;
+                        if constexpr (I64) {
+                            unsigned long long t0, t1 = 0;
+                            asm volatile("ld.shared.u64 %0, [%1];" : "=l"(t0) : "r"(kb + swz<LBK>((uint32_t)(g * LBK + lane * 8))));
+                            if (lane > 0)
+                                asm volatile("ld.shared.u64 %0, [%1];" : "=l"(t1) : "r"(kb + swz<LBK>((uint32_t)(g * LBK + (lane - 1) * 8))));
+                            kc = (long long)t0;
+                            kq = (long long)t1;
+                        } else {
+                            int t0, t1 = 0;
+                            asm volatile("ld.shared.s32 %0, [%1];" : "=r"(t0) : "r"(kb + swz<LBK>((uint32_t)(g * LBK + lane * 4))));
+                            if (lane > 0)
+                                asm volatile("ld.shared.s32 %0, [%1];" : "=r"(t1) : "r"(kb + swz<LBK>((uint32_t)(g * LBK + (lane - 1) * 4))));
+                            kc = t0;
+                            kq = t1;
+                        }
+                    } else {
+                        kc = key_at(gr0 + lane);
+                        kq = lane > 0 ? key_at(gr0 + lane - 1) : 0;
+                    }
+                    if (lane == 0) kq = (long long)gkp;
+                    if (kc - kq > 1) gap_fill(kq, kc);
                 }
+            }
         }
 
         // ---- warp pass: segmented inclusive scan of the lane tails (Alg. 1 analog)
@@ -374,32 +467,54 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, 2) narrow_kernel(const Narr
         const bool cont = nv > 0 && !(hm & 1u);
         const int j = hm ? (__ffs(hm) - 2) : (last_ends ? nv - 1 : -1);
         if (cont && j >= 0) {
-            // the lane's partial at item j, via the per-warp shared-memory copy
-            float4* mine = &s_acc[warp][0][lane];
-#pragma unroll
-            for (int q = 0; q < NQ; ++q) {
-                float4 t;
-                t.x = acc[(4 * q + 0) / F][(4 * q + 0) % F];
-                t.y = (4 * q + 1 < NACC) ? acc[(4 * q + 1) / F][(4 * q + 1) % F] : 0.f;
-                t.z = (4 * q + 2 < NACC) ? acc[(4 * q + 2) / F][(4 * q + 2) % F] : 0.f;
-                t.w = (4 * q + 3 < NACC) ? acc[(4 * q + 3) / F][(4 * q + 3) % F] : 0.f;
-                mine[q * 32] = t;
-            }
-            const float* sp = reinterpret_cast<const float*>(&s_acc[warp][0][0]);
+            // the lane's partial at item j (a dynamic index)
             float tot[F];
+            if constexpr (ESZ == 4) {
+                // fp32: the lane's partials have exactly the shape of its value row,
+                // whose ring slot it has already consumed: write them there (same
+                // swizzled layout, conflict-free) and read item j back
+                const uint32_t vb = ring + b * STAGE;
 #pragma unroll
-            for (int f = 0; f < F; ++f) {
-                const int e = j * F + f;  // element e of the lane's partials: piece e/4, word e%4
-                tot[f] = nfold<OP>(cin[f], sp[((e >> 2) * 32 + lane) * 4 + (e & 3)]);
+                for (int q = 0; q < LBV / 16; ++q) {
+                    const uint32_t o = vb + swz<LBV>((uint32_t)(lane * LBV + q * 16));
+                    asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(o),
+                                 "f"(acc[(4 * q + 0) / F][(4 * q + 0) % F]), "f"(acc[(4 * q + 1) / F][(4 * q + 1) % F]),
+                                 "f"(acc[(4 * q + 2) / F][(4 * q + 2) % F]), "f"(acc[(4 * q + 3) / F][(4 * q + 3) % F])
+                                 : "memory");
+                }
+#pragma unroll
+                for (int f = 0; f < F; ++f) {
+                    float t;
+                    asm volatile("ld.shared.f32 %0, [%1];"
+                                 : "=f"(t)
+                                 : "r"(vb + swz<LBV>((uint32_t)(lane * LBV + (j * F + f) * 4)))
+                                 : "memory");
+                    tot[f] = nfold<OP>(cin[f], t);
+                }
+            } else {  // bf16: the partials are twice the row; select chain
+#pragma unroll
+                for (int f = 0; f < F; ++f) tot[f] = acc[0][f];
+#pragma unroll
+                for (int i = 1; i < ITEMS; ++i)
+#pragma unroll
+                    for (int f = 0; f < F; ++f) tot[f] = (i == j) ? acc[i][f] : tot[f];
+#pragma unroll
+                for (int f = 0; f < F; ++f) tot[f] = nfold<OP>(cin[f], tot[f]);
             }
             if (creach && rhead) {  // the agent's head segment: resolved below
 #pragma unroll
                 for (int f = 0; f < F; ++f) hacc[f] = tot[f];
                 head_end = r0 + j + 1;
             } else {
-                store_at(k[0], tot, (int)((r0 - e_lo) + j + 1 - cpos));
+                store_at(true, k[0], tot, (int)((r0 - e_lo) + j + 1 - cpos));
             }
         }
+
+        // ---- release the stage (all lanes are done with it) and refill it: the
+        // proxy fence orders this chunk's shared-memory accesses before the refill
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0 && s + NS < nring) issue(s + NS);
 
         // ---- running segment for the next chunk: the last valid lane's state
         const unsigned vmask = __ballot_sync(0xffffffffu, nv > 0);
@@ -456,7 +571,7 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, 2) narrow_kernel(const Narr
             for (int f = 0; f < F; ++f) tot[f] = nfold<OP>(tot[f], ld_cg_f32(p.carry_h + m * F + f));
 #pragma unroll
         for (int f = 0; f < F; ++f) tot[f] = nfold<OP>(tot[f], hacc[f]);
-        store_at((KT)first_key, tot, (int)(head_end - ld_volatile_i64(&p.meta[u].tail_start)));
+        store_at(true, (KT)first_key, tot, (int)(head_end - ld_volatile_i64(&p.meta[u].tail_start)));
     }
     __syncthreads();
     if (threadIdx.x == 0) {
