@@ -36,11 +36,18 @@ __device__ __forceinline__ uint16_t ld_stream(const uint16_t* p) {
     asm("ld.global.nc.L1::no_allocate.u16 %0, [%1];" : "=h"(r) : "l"(p));
     return r;
 }
+__device__ __forceinline__ uint2 ld_stream(const uint2* p) {
+    uint2 r;
+    asm("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+    return r;
+}
 __device__ __forceinline__ uint4 ld_cached(const uint4* p) { return __ldg(p); }
+__device__ __forceinline__ uint2 ld_cached(const uint2* p) { return __ldg(p); }
 __device__ __forceinline__ uint32_t ld_cached(const uint32_t* p) { return __ldg(p); }
 __device__ __forceinline__ uint16_t ld_cached(const uint16_t* p) { return __ldg(p); }
 
 __device__ __forceinline__ void st_vec(uint4* p, uint4 v) { *p = v; }
+__device__ __forceinline__ void st_vec(uint2* p, uint2 v) { *p = v; }
 __device__ __forceinline__ void st_vec(uint32_t* p, uint32_t v) { *p = v; }
 __device__ __forceinline__ void st_vec(uint16_t* p, uint16_t v) { *p = v; }
 
@@ -95,6 +102,42 @@ struct Conv<__nv_bfloat16, 8> {
 #pragma unroll
         for (int i = 0; i < 4; ++i) w[i] = (uint32_t)f2bf_bits(f[2 * i]) | ((uint32_t)f2bf_bits(f[2 * i + 1]) << 16);
         return make_uint4(w[0], w[1], w[2], w[3]);
+    }
+};
+template <>
+struct Conv<float, 2> {
+    using Raw = uint2;
+    __device__ __forceinline__ static void unpack(const Raw& r, float (&f)[2]) {
+        f[0] = __uint_as_float(r.x);
+        f[1] = __uint_as_float(r.y);
+    }
+    __device__ __forceinline__ static Raw pack(const float (&f)[2]) {
+        return make_uint2(__float_as_uint(f[0]), __float_as_uint(f[1]));
+    }
+};
+template <>
+struct Conv<__nv_bfloat16, 4> {
+    using Raw = uint2;
+    __device__ __forceinline__ static void unpack(const Raw& r, float (&f)[4]) {
+        f[0] = __uint_as_float(r.x << 16);
+        f[1] = __uint_as_float(r.x & 0xFFFF0000u);
+        f[2] = __uint_as_float(r.y << 16);
+        f[3] = __uint_as_float(r.y & 0xFFFF0000u);
+    }
+    __device__ __forceinline__ static Raw pack(const float (&f)[4]) {
+        return make_uint2((uint32_t)f2bf_bits(f[0]) | ((uint32_t)f2bf_bits(f[1]) << 16),
+                          (uint32_t)f2bf_bits(f[2]) | ((uint32_t)f2bf_bits(f[3]) << 16));
+    }
+};
+template <>
+struct Conv<__nv_bfloat16, 2> {
+    using Raw = uint32_t;
+    __device__ __forceinline__ static void unpack(const Raw& r, float (&f)[2]) {
+        f[0] = __uint_as_float(r << 16);
+        f[1] = __uint_as_float(r & 0xFFFF0000u);
+    }
+    __device__ __forceinline__ static Raw pack(const float (&f)[2]) {
+        return (uint32_t)f2bf_bits(f[0]) | ((uint32_t)f2bf_bits(f[1]) << 16);
     }
 };
 template <>
@@ -207,6 +250,24 @@ template <>
 __device__ __forceinline__ uint4 lds_vec<uint4>(uint32_t addr) {
     uint4 r;
     asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(addr));
+    return r;
+}
+template <>
+__device__ __forceinline__ uint2 lds_vec<uint2>(uint32_t addr) {
+    uint2 r;
+    asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "r"(addr));
+    return r;
+}
+template <>
+__device__ __forceinline__ uint32_t lds_vec<uint32_t>(uint32_t addr) {
+    uint32_t r;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(r) : "r"(addr));
+    return r;
+}
+template <>
+__device__ __forceinline__ uint16_t lds_vec<uint16_t>(uint32_t addr) {
+    uint16_t r;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(r) : "r"(addr));
     return r;
 }
 

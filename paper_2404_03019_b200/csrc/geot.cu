@@ -174,12 +174,7 @@ static geot_status resolve_config(long long nnz, long long S, long long F, geot_
             c.ctas_per_sm = 0;
         }
         if (user->variant == GEOT_VARIANT_STREAM && c.variant != GEOT_VARIANT_STREAM) {
-            if (!stream_eligible(nnz, F, dt, fused, c)) return GEOT_ERR_UNSUPPORTED;
-            c.variant = GEOT_VARIANT_STREAM;
-            c.rows_per_group = stream_rows_per_stage(F, dt, c.lanes_per_row, c.vecs_per_lane);
-            c.warps_per_cta = stream_warps(c.vecs_per_lane);
-            c.stages = stream_stages(c.vecs_per_lane);
-            c.ctas_per_sm = 1;
+            if (!stream_eligible(nnz, F, dt, fused) || !to_stream(F, dt, &c)) return GEOT_ERR_UNSUPPORTED;
         }
         if (c.variant == GEOT_VARIANT_STREAM) {  // lane shape fixed by F; pipeline shape tunable
             if (user->rows_per_group) c.rows_per_group = user->rows_per_group;
@@ -255,7 +250,7 @@ static geot_status reduce_common(const void* X, long long V, const void* src_idx
     st = resolve_config(nnz, S, F, op, dt, it, mode >= 1, user_cfg, &c);
     if (st != GEOT_OK) return st;
     // vector path needs 16-byte aligned row starts of the value/output arrays
-    if (c.vec_elems > 1 && !(aligned(X, 16) && aligned(out, 16))) {
+    if ((c.vec_elems > 1 || c.variant == GEOT_VARIANT_STREAM) && !(aligned(X, 16) && aligned(out, 16))) {
         if (user_cfg && (user_cfg->vec_elems > 1 || user_cfg->variant == GEOT_VARIANT_STREAM))
             return GEOT_ERR_UNSUPPORTED;
         c.variant = GEOT_VARIANT_EDGE_TILE;
@@ -333,9 +328,9 @@ static geot_status reduce_common(const void* X, long long V, const void* src_idx
             fx.F = (int)F;
             fx.op = (int)op;
             cudaError_t e = dt == GEOT_F32
-                                ? launch_stream_f32(sp, fx, c.lanes_per_row, c.vecs_per_lane, c.warps_per_cta,
+                                ? launch_stream_f32(sp, fx, c.vec_elems, c.lanes_per_row, c.vecs_per_lane, c.warps_per_cta,
                                                     c.rows_per_group, c.stages == 1 ? 0 : c.stages, op == GEOT_MAX, nsm, stream)
-                                : launch_stream_bf16(sp, fx, c.lanes_per_row, c.vecs_per_lane, c.warps_per_cta,
+                                : launch_stream_bf16(sp, fx, c.vec_elems, c.lanes_per_row, c.vecs_per_lane, c.warps_per_cta,
                                                      c.rows_per_group, c.stages == 1 ? 0 : c.stages, op == GEOT_MAX, nsm, stream);
             if (e == cudaErrorNotSupported) return GEOT_ERR_UNSUPPORTED;
             return from_cuda(e);
@@ -343,6 +338,8 @@ static geot_status reduce_common(const void* X, long long V, const void* src_idx
         // too few rows for one per agent: edge-tile kernel with its own shape
         c.variant = GEOT_VARIANT_EDGE_TILE;
         c.ctas_per_sm = 0;
+        const int wide = dt == GEOT_F32 ? 4 : 8;
+        c.vec_elems = (F % wide == 0) ? wide : 1;  // the edge-tile kernel's vector widths
         select_shape_for_vw(F, dt, &c);
     }
     const long long ntiles = ntiles_of(nnz, c);

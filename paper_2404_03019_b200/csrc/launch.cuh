@@ -117,9 +117,8 @@ cudaError_t run_edge_tile(const EdgeTileParams& p, int ctas_per_sm, int nsm, cud
 // agent owns >= 1 row).  Agent count = carry slots.
 long long stream_agents(long long nnz, int lpr, int warps, int nsm, int ctas_per_sm);
 
-template <typename T, int LPR, int VPL, bool ISMAX, int W, int RS, int NS>
+template <typename T, int VW, int LPR, int VPL, bool ISMAX, int W, int RS, int NS>
 cudaError_t run_stream(const StreamParams& p, const EdgeTileParams& fix, int nsm, cudaStream_t st) {
-    constexpr int VW = 16 / (int)sizeof(T);
     constexpr int G = 32 / LPR;
     auto kern = stream_kernel<T, VW, LPR, VPL, ISMAX, W, RS, NS>;
     const size_t smem = stream_smem_bytes(W, NS, G, RS, p.row_bytes);
@@ -140,14 +139,18 @@ cudaError_t run_stream(const StreamParams& p, const EdgeTileParams& fix, int nsm
 }
 
 // Compiled (lane shape) x (pipeline shape W warps / RS rows per stage / NS
-// stages).  The first pipeline listed for a lane shape is its default.
+// stages).  Lane shapes: 16-byte lane vectors, LPR lanes per row (32/LPR
+// agents per warp), VPL vectors per lane; the first pipeline listed for a lane
+// shape is its default (stream_default_pipe in select.cpp mirrors it).
 template <typename T>
-cudaError_t launch_stream(const StreamParams& p, const EdgeTileParams& fix, int lpr, int vpl, int w, int rs, int ns,
-                          bool ismax, int nsm, cudaStream_t st) {
-#define GEOT_SSHAPE(LPR_, VPL_, W_, RS_, NS_)                                                         \
-    if (lpr == LPR_ && vpl == VPL_ && w == W_ && rs == RS_ && ns == NS_)                              \
-        return ismax ? run_stream<T, LPR_, VPL_, true, W_, RS_, NS_>(p, fix, nsm, st)                 \
-                     : run_stream<T, LPR_, VPL_, false, W_, RS_, NS_>(p, fix, nsm, st);
+cudaError_t launch_stream(const StreamParams& p, const EdgeTileParams& fix, int vw, int lpr, int vpl, int w, int rs,
+                          int ns, bool ismax, int nsm, cudaStream_t st) {
+    constexpr int WIDE = 16 / (int)sizeof(T);
+    if (vw != WIDE) return cudaErrorNotSupported;
+#define GEOT_SSHAPE(LPR_, VPL_, W_, RS_, NS_)                                                        \
+    if (lpr == LPR_ && vpl == VPL_ && w == W_ && rs == RS_ && ns == NS_)                             \
+        return ismax ? run_stream<T, WIDE, LPR_, VPL_, true, W_, RS_, NS_>(p, fix, nsm, st)          \
+                     : run_stream<T, WIDE, LPR_, VPL_, false, W_, RS_, NS_>(p, fix, nsm, st);
 #define GEOT_SSHAPE_V1(LPR_)         \
     GEOT_SSHAPE(LPR_, 1, 16, 6, 4)   \
     GEOT_SSHAPE(LPR_, 1, 8, 6, 8)    \
@@ -188,8 +191,10 @@ struct NarrowParams;
 cudaError_t launch_narrow(const NarrowParams& p, int F, bool bf16, bool ismax, bool i64, int nsm, cudaStream_t st);
 long long narrow_agents_max(int nsm);
 
-cudaError_t launch_stream_f32(const StreamParams&, const EdgeTileParams&, int, int, int, int, int, bool, int, cudaStream_t);
-cudaError_t launch_stream_bf16(const StreamParams&, const EdgeTileParams&, int, int, int, int, int, bool, int, cudaStream_t);
+cudaError_t launch_stream_f32(const StreamParams&, const EdgeTileParams&, int, int, int, int, int, int, bool, int,
+                              cudaStream_t);
+cudaError_t launch_stream_bf16(const StreamParams&, const EdgeTileParams&, int, int, int, int, int, int, bool, int,
+                               cudaStream_t);
 
 // Switch over the compiled (VW, LPR, VPL, ISMAX) set for one (T, MODE).
 // Compiled shapes: LPR in {1,2,4,8,16,32} with VPL = 1, and LPR = 32 with

@@ -13,11 +13,13 @@ geot_status select_config_impl(long long nnz, long long S, long long F, geot_red
 // Derive the lane shape (LPR, VPL) and rows-per-group for c->vec_elems.
 void select_shape_for_vw(long long F, geot_dtype dt, geot_config* c);
 
-// GEOT_VARIANT_STREAM applicability and its rows per ring stage.
-bool stream_eligible(long long nnz, long long F, geot_dtype dt, int fused, const geot_config& c);
-int stream_rows_per_stage(long long F, geot_dtype dt, int lpr, int vpl);
+// GEOT_VARIANT_STREAM: applicability, lane shape (16-byte lane vectors), the
+// compiled pipelines, and switching a configuration to its default pipeline.
+bool stream_eligible(long long nnz, long long F, geot_dtype dt, int fused);
+bool stream_lane_shape(long long F, geot_dtype dt, int* lpr, int* vpl);
+bool stream_pipe_compiled(int lpr, int vpl, geot_dtype dt, int w, int rs, int ns);
+bool to_stream(long long F, geot_dtype dt, geot_config* c);
 bool narrow_eligible(long long nnz, long long F, geot_dtype dt, int fused);
-bool stream_pipe_compiled(int lpr, int vpl, int w, int rs, int ns);
 
 // The generated tree itself (diagnostics / codegen-fidelity test) and its provenance.
 void select_tree_raw(double log2_nnz, double avg, double F, double dtype, double fused, int out[4]);

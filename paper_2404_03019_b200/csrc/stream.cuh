@@ -34,6 +34,13 @@ __host__ __device__ constexpr int stream_warps(int vpl) { return vpl >= 4 ? 8 : 
 __host__ __device__ constexpr int stream_rs(int vpl) { return vpl == 1 ? 6 : (vpl == 8 ? 1 : 3); }
 __host__ __device__ constexpr int stream_stages(int vpl) { return 4 + 0 * vpl; }
 
+// Rows per unrolled sub-chunk of a stage: the largest divisor of RS <= 8.
+__host__ __device__ constexpr int stream_sub(int rs) {
+    int d = rs < 8 ? rs : 8;
+    while (rs % d) --d;
+    return d;
+}
+
 // Control words in the workspace (zero-filled once before first use; the last
 // CTA of every call re-arms ticket/done and advances the epoch, so per-agent
 // flags published in a call (value epoch+1) never need clearing).
@@ -77,8 +84,11 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
     constexpr int G = 32 / LPR;
     using Cv = Conv<T, VW>;
     using Raw = typename Cv::Raw;
-    static_assert(sizeof(Raw) == 16, "stream kernel moves 16-byte vectors");
+    constexpr int SUB = stream_sub(RS);  // rows per unrolled sub-chunk (LDG path: RS <= 8)
+    static_assert(NS > 0 || SUB == RS, "the LDG pipeline holds whole stages in registers");
+    constexpr int VB = (int)sizeof(Raw);  // bytes per lane vector (2..16; one agent per warp below 16)
     static_assert(RS <= LPR, "one key per lane per stage");
+    static_assert(VB == 16 || LPR == 32, "narrow lane vectors: one agent per warp");
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -233,16 +243,17 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
 #pragma unroll
     for (int j = 0; j < VPL; ++j) col_ok[j] = vec_col(j) < p.NV;
     // one stage of RS rows (already in registers) + this lane's key (row li)
-    auto process = [&](const Raw (&rows)[RS][VPL], long long kmine, long long kprev, int cnt, long long r_base) {
-        // is_seg of the whole stage (Alg. 1): row r starts a segment iff its
-        // key differs from row r-1's (row -1: `cur`)
-        const unsigned heads = __ballot_sync(gmask, li < cnt && kmine != kprev) >> (gi * LPR);
+    // SUB rows at a time (code size: the segment-end path is inlined once per
+    // row of a sub-chunk); `heads` bit r = row r starts a segment; the key of
+    // row r is held by lane (koff + r) of the group
+    auto process = [&](const Raw (&rows)[SUB][VPL], unsigned heads, long long kmine, int koff, int cnt,
+                       long long r_base) {
 #pragma unroll
-        for (int r = 0; r < RS; ++r) {
+        for (int r = 0; r < SUB; ++r) {
             if (r >= cnt) break;
             const Raw (&raw)[VPL] = rows[r];
             if ((heads >> r) & 1u) {  // segment `cur` ended at the previous row
-                const long long k = __shfl_sync(gmask, kmine, r, LPR);
+                const long long k = __shfl_sync(gmask, kmine, koff + r, LPR);
                 const long long e = r_base + r;
                 if (first && head_open) {
 #pragma unroll
@@ -275,7 +286,7 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
 
     if constexpr (TMA) {
         // 32-bit shared address of this lane's first vector in group gi's rows of buffer 0
-        const uint32_t lane_s0 = smem_u32(wbuf) + gi * RS * row_bytes + li * 16;
+        const uint32_t lane_s0 = smem_u32(wbuf) + gi * RS * row_bytes + li * VB;
 #pragma unroll 1
         for (int s = 0; s < nst_w; ++s) {
             const int b = s % NSX;
@@ -285,22 +296,43 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
             const long long r_base = e_lo + (long long)s * RS;
             int cnt = (int)(e_hi - r_base);
             cnt = cnt < 0 ? 0 : (cnt > RS ? RS : cnt);
-            // the whole stage's rows into registers at once (RS x VPL x 16 B per lane)
-            Raw rows[RS][VPL];
-#pragma unroll
-            for (int r = 0; r < RS; ++r)
-#pragma unroll
-                for (int j = 0; j < VPL; ++j)
-                    rows[r][j] = (r < cnt && col_ok[j]) ? lds_vec<Raw>(sbase + r * row_bytes + j * LPR * 16) : Raw{};
             const long long kmine = (li < cnt) ? gkey[li] : KEY_AFTER;
             const long long kprev = (li == 0) ? cur : ((li <= cnt) ? gkey[li - 1] : KEY_AFTER);
-            // the stage now lives in registers: hand its buffer back to the TMA
-            // producer right away (the proxy fence orders these shared-memory
-            // reads before the async-proxy writes of the refill)
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            __syncwarp();
-            if (s + NSX < nst_w) issue(s + NSX);
-            process(rows, kmine, kprev, cnt, r_base);
+            // is_seg of the whole stage (Alg. 1): row r starts a segment iff its
+            // key differs from row r-1's (row -1: `cur`)
+            const unsigned heads = __ballot_sync(gmask, li < cnt && kmine != kprev) >> (gi * LPR);
+            if constexpr (SUB == RS) {
+                // the whole stage's rows into registers at once, then hand the buffer
+                // back to the TMA producer right away (the proxy fence orders these
+                // shared-memory reads before the async-proxy writes of the refill)
+                Raw rows[SUB][VPL];
+#pragma unroll
+                for (int r = 0; r < SUB; ++r)
+#pragma unroll
+                    for (int j = 0; j < VPL; ++j)
+                        rows[r][j] = (r < cnt && col_ok[j]) ? lds_vec<Raw>(sbase + r * row_bytes + j * LPR * VB) : Raw{};
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (s + NSX < nst_w) issue(s + NSX);
+                process(rows, heads, kmine, 0, cnt, r_base);
+            } else {
+                // large stages of small rows: SUB rows at a time, buffer released after
+#pragma unroll 1
+                for (int r0 = 0; r0 < cnt; r0 += SUB) {
+                    Raw rows[SUB][VPL];
+#pragma unroll
+                    for (int r = 0; r < SUB; ++r)
+#pragma unroll
+                        for (int j = 0; j < VPL; ++j)
+                            rows[r][j] = (r0 + r < cnt && col_ok[j])
+                                             ? lds_vec<Raw>(sbase + (r0 + r) * row_bytes + j * LPR * VB)
+                                             : Raw{};
+                    process(rows, heads >> r0, kmine, r0, cnt - r0, r_base + r0);
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (s + NSX < nst_w) issue(s + NSX);
+            }
         }
     } else {
         // LDG path: the next stage's rows and key are loaded into registers
@@ -336,7 +368,8 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
             cnt = cnt > RS ? RS : cnt;
             long long kprev = __shfl_up_sync(gmask, kmine, 1, LPR);
             if (li == 0) kprev = cur;
-            process(rows, kmine, kprev, cnt, r_base);
+            const unsigned heads = __ballot_sync(gmask, li < cnt && kmine != kprev) >> (gi * LPR);
+            process(rows, heads, kmine, 0, cnt, r_base);
         }
     }
 

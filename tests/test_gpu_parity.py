@@ -164,7 +164,7 @@ def test_narrow_variant(geot, F, dtype, op):
 @pytest.mark.parametrize("kind", synth.STRESS_KINDS)
 @pytest.mark.parametrize("itype", ["i32", "i64"])
 def test_narrow_stress(geot, kind, itype):
-    for F in (1, 4):
+    for F in (1, 4, 8):
         for op in ("sum", "mean", "max"):
             parity(geot, 150_001, 12_000, F, op, "f32", "int", kind, seed=5, itype=itype, cfg={"variant": NARROW})
 

@@ -58,8 +58,11 @@ def test_codegen_matches_tree(L):
     assert L.geot_selector_provenance().startswith(b"B200 refit")
 
 
-STREAM_PIPES = {1: {(16, 6, 4), (8, 6, 8), (16, 3, 8), (8, 8, 6)}, 2: {(16, 3, 4), (8, 3, 8)}, 4: {(8, 3, 4)},
-                8: {(8, 1, 4), (8, 1, 6)}}
+# compiled stream pipelines (warps, rows per stage, stages) per vectors per lane (launch.cuh);
+# stages 1 = the LDG register pipeline
+STREAM_PIPES = {1: {(16, 6, 4), (8, 6, 8), (16, 3, 8), (8, 8, 6), (8, 4, 1), (8, 8, 1)},
+                2: {(16, 3, 4), (8, 3, 8), (8, 4, 1)}, 4: {(8, 3, 4), (8, 2, 1)},
+                8: {(8, 1, 4), (8, 1, 6), (8, 1, 1)}}
 
 
 def test_select_config_always_valid(L):
@@ -73,11 +76,12 @@ def test_select_config_always_valid(L):
                         S = max(1, nnz // avg)
                         assert L.geot_select_config(nnz, S, F, 0, dt, 0, fused, ctypes.byref(c)) == 0
                         wide = 4 if dt == 0 else 8
-                        if c.variant == 3:
+                        if c.variant == 3:  # 16-byte lane vectors, 8/16/32 lanes per row
                             assert not fused and c.vec_elems == wide and c.lanes_per_row >= 8
+                            assert F // wide <= c.lanes_per_row * c.vecs_per_lane
                             assert (c.warps_per_cta, c.rows_per_group, c.stages) in STREAM_PIPES[c.vecs_per_lane]
                         elif c.variant == 2:
-                            assert not fused and F * (4 if dt == 0 else 2) <= 32
+                            assert not fused and (F in (1, 2, 4, 8) or (dt == 1 and F == 16))
                         else:
                             assert c.variant == 1 and 1 <= c.rows_per_group <= 1024
                             assert c.vec_elems in (1, wide) and F % c.vec_elems == 0

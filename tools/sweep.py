@@ -68,9 +68,25 @@ def make_inputs(E, S, F, dtype, dist, seed, fused=False, V=None, itype=torch.int
     return L, idx, X, None
 
 
+# compiled stream pipelines per vectors per lane — launch.cuh
 STREAM_PIPES = {1: [(16, 6, 4), (8, 6, 8), (16, 3, 8), (8, 8, 6), (8, 4, 1), (8, 8, 1)],
                 2: [(16, 3, 4), (8, 3, 8), (8, 4, 1)], 4: [(8, 3, 4), (8, 2, 1)],
                 8: [(8, 1, 4), (8, 1, 6), (8, 1, 1)]}
+
+
+def stream_lane_shape(F, dtype):
+    """(lanes per row, vectors per lane) of the stream kernel for F, or None (select.cpp)."""
+    wide = 4 if dtype == "f32" else 8
+    if F % wide or F // wide < 8:
+        return None
+    nv = F // wide
+    lpr = 8
+    while lpr < nv and lpr < 32:
+        lpr *= 2
+    v = 1
+    while lpr * v < nv:
+        v *= 2
+    return (lpr, v) if v <= (8 if dtype == "f32" else 4) else None
 
 
 def candidate_configs(E, S, F, dtype, fused, quick=False):
@@ -84,15 +100,13 @@ def candidate_configs(E, S, F, dtype, fused, quick=False):
     # eligibility from the input alone (not from the current selection)
     esz = 4 if dtype == "f32" else 2
     narrow_ok = (not fused) and E >= 65536 and (F in (1, 2, 4, 8) or (dtype == "bf16" and F == 16))
-    nv = F * esz // 16 if (F * esz) % 16 == 0 else 0
-    lpr = 32 if nv >= 32 else (1 << max(0, (nv - 1).bit_length())) if nv else 0
-    vpl = 1 if nv <= 32 else min(8 if dtype == "f32" else 4, 1 << ((nv + 31) // 32 - 1).bit_length())
-    stream_ok = (not fused) and E >= 65536 and nv > 0 and lpr >= 8 and nv <= lpr * vpl
+    shape = stream_lane_shape(F, dtype)
+    stream_ok = (not fused) and E >= 65536 and shape is not None
     if narrow_ok:
         out.append({"variant": 2})
     if stream_ok:
-        for (w, rs, ns) in STREAM_PIPES.get(vpl, []):
-            if rs <= lpr:
+        for (w, rs, ns) in STREAM_PIPES[shape[1]]:
+            if rs <= shape[0]:
                 out.append({"variant": 3, "warps_per_cta": w, "rows_per_group": rs, "stages": ns})
     return base, out
 
