@@ -316,6 +316,9 @@ static geot_status reduce_common(const void* X, long long V, const void* src_idx
             sp.row_bytes = (int)(F * (long long)esz);
             sp.op = (int)op;
             sp.idx64 = it == GEOT_I64;
+            sp.src = src_idx;
+            sp.w = w;
+            sp.V = V;
             EdgeTileParams fx{};
             fx.out = out;
             fx.meta = sp.meta;
@@ -327,7 +330,15 @@ static geot_status reduce_common(const void* X, long long V, const void* src_idx
             fx.ntiles = NA;
             fx.F = (int)F;
             fx.op = (int)op;
-            cudaError_t e = dt == GEOT_F32
+            const int ns = c.stages == 1 ? 0 : c.stages;
+            cudaError_t e;
+            if (mode >= 1)
+                e = dt == GEOT_F32 ? launch_stream_gather_f32(sp, fx, c.lanes_per_row, c.vecs_per_lane, c.warps_per_cta,
+                                                              c.rows_per_group, ns, op == GEOT_MAX, mode, nsm, stream)
+                                   : launch_stream_gather_bf16(sp, fx, c.lanes_per_row, c.vecs_per_lane, c.warps_per_cta,
+                                                               c.rows_per_group, ns, op == GEOT_MAX, mode, nsm, stream);
+            else
+                e = dt == GEOT_F32
                                 ? launch_stream_f32(sp, fx, c.vec_elems, c.lanes_per_row, c.vecs_per_lane, c.warps_per_cta,
                                                     c.rows_per_group, c.stages == 1 ? 0 : c.stages, op == GEOT_MAX, nsm, stream)
                                 : launch_stream_bf16(sp, fx, c.vec_elems, c.lanes_per_row, c.vecs_per_lane, c.warps_per_cta,

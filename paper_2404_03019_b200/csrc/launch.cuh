@@ -117,11 +117,11 @@ cudaError_t run_edge_tile(const EdgeTileParams& p, int ctas_per_sm, int nsm, cud
 // agent owns >= 1 row).  Agent count = carry slots.
 long long stream_agents(long long nnz, int lpr, int warps, int nsm, int ctas_per_sm);
 
-template <typename T, int VW, int LPR, int VPL, bool ISMAX, int W, int RS, int NS>
+template <typename T, int VW, int LPR, int VPL, bool ISMAX, int W, int RS, int NS, int MODE = 0, bool SRC64 = false>
 cudaError_t run_stream(const StreamParams& p, const EdgeTileParams& fix, int nsm, cudaStream_t st) {
     constexpr int G = 32 / LPR;
-    auto kern = stream_kernel<T, VW, LPR, VPL, ISMAX, W, RS, NS>;
-    const size_t smem = stream_smem_bytes(W, NS, G, RS, p.row_bytes);
+    auto kern = stream_kernel<T, VW, LPR, VPL, ISMAX, W, RS, NS, MODE, SRC64>;
+    const size_t smem = stream_smem_bytes(W, NS, G, RS, p.row_bytes, MODE);
     if (smem > 227 * 1024) return cudaErrorNotSupported;
     const int occ = cached_occupancy(kern, W * 32, smem);
     if (occ < (NS > 0 ? 1 : 2)) return cudaErrorInvalidConfiguration;  // agents assume this many CTAs/SM
@@ -175,6 +175,37 @@ cudaError_t launch_stream(const StreamParams& p, const EdgeTileParams& fix, int 
 #undef GEOT_SSHAPE
     return cudaErrorNotSupported;
 }
+// Fused gather forms through the stream kernel (MODE 1: x[src[e]], 2: w[e] *
+// x[src[e]]): 16-byte lane vectors, one vector per lane, two pipelines per lane shape.
+template <typename T>
+cudaError_t launch_stream_gather(const StreamParams& p, const EdgeTileParams& fix, int lpr, int vpl, int w, int rs,
+                                 int ns, bool ismax, int mode, int nsm, cudaStream_t st) {
+    constexpr int WIDE = 16 / (int)sizeof(T);
+    if (vpl != 1 || (mode != 1 && mode != 2)) return cudaErrorNotSupported;
+#define GEOT_GSHAPE_I(LPR_, W_, RS_, NS_, I64_)                                                                \
+    if (mode == 2) return run_stream<T, WIDE, LPR_, 1, false, W_, RS_, NS_, 2, I64_>(p, fix, nsm, st);          \
+    return ismax ? run_stream<T, WIDE, LPR_, 1, true, W_, RS_, NS_, 1, I64_>(p, fix, nsm, st)                   \
+                 : run_stream<T, WIDE, LPR_, 1, false, W_, RS_, NS_, 1, I64_>(p, fix, nsm, st);
+#define GEOT_GSHAPE(LPR_, W_, RS_, NS_)                                                                        \
+    if (lpr == LPR_ && w == W_ && rs == RS_ && ns == NS_) {                                                    \
+        if (p.idx64) {                                                                                         \
+            GEOT_GSHAPE_I(LPR_, W_, RS_, NS_, true)                                                            \
+        } else {                                                                                               \
+            GEOT_GSHAPE_I(LPR_, W_, RS_, NS_, false)                                                           \
+        }                                                                                                      \
+    }
+    GEOT_GSHAPE(8, 16, 6, 4)
+    GEOT_GSHAPE(16, 16, 6, 4)
+    GEOT_GSHAPE(32, 16, 6, 4)
+#undef GEOT_GSHAPE_I
+#undef GEOT_GSHAPE
+    return cudaErrorNotSupported;
+}
+cudaError_t launch_stream_gather_f32(const StreamParams&, const EdgeTileParams&, int, int, int, int, int, bool, int,
+                                     int, cudaStream_t);
+cudaError_t launch_stream_gather_bf16(const StreamParams&, const EdgeTileParams&, int, int, int, int, int, bool, int,
+                                      int, cudaStream_t);
+
 // gradients (backward.cu)
 cudaError_t launch_segment_backward(const void* dY, const void* idx, int idx64, long long E, long long seg_base,
                                     long long S, int F, int op, int bf16, const long long* offsets, const void* X,

@@ -17,7 +17,7 @@ void select_shape_for_vw(long long F, geot_dtype dt, geot_config* c);
 // compiled pipelines, and switching a configuration to its default pipeline.
 bool stream_eligible(long long nnz, long long F, geot_dtype dt, int fused);
 bool stream_lane_shape(long long F, geot_dtype dt, int* lpr, int* vpl);
-bool stream_pipe_compiled(int lpr, int vpl, geot_dtype dt, int w, int rs, int ns);
+bool stream_pipe_compiled(int lpr, int vpl, geot_dtype dt, int w, int rs, int ns, int fused);
 bool to_stream(long long F, geot_dtype dt, geot_config* c);
 bool narrow_eligible(long long nnz, long long F, geot_dtype dt, int fused);
 

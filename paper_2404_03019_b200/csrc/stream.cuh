@@ -66,20 +66,42 @@ struct StreamParams {
     int row_bytes;     // F * sizeof(T)
     int op;
     int idx64;
+    // fused forms (MODE 1/2): row e's data is x[src[e], :] (x has V rows), times w[e]
+    const void* src;
+    const float* w;
+    long long V;
 };
 
-__host__ __device__ inline size_t stream_smem_bytes(int W, int NS, int G, int RS, int row_bytes) {
+__host__ __device__ inline size_t stream_smem_bytes(int W, int NS, int G, int RS, int row_bytes, int mode = 0) {
     return (size_t)W * NS * G * RS * row_bytes       // row ring
            + (size_t)W * NS * G * RS * 8             // key ring
-           + (size_t)W * NS * 8;                     // mbarriers
+           + (size_t)W * NS * 8                      // mbarriers
+           + (mode == 2 ? (size_t)W * NS * G * RS * 4 : 0)   // weight ring
+           + (mode >= 1 ? (size_t)W * NS * G * RS * 8 : 0);  // src-id ring (NS stages ahead)
 }
+
+// cp.async of 16 bytes; src_bytes 0 zero-fills the destination (no global read)
+__device__ __forceinline__ void cp_async_16_zfill(uint32_t dst, const void* src, uint32_t src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+
 
 // NS > 0: TMA bulk-copy ring of NS stages per warp (one CTA per SM).
 // NS == 0: the same agents and carries, rows streamed with 128-bit LDG into a
 //          register double buffer (several CTAs per SM, no shared ring).
-template <typename T, int VW, int LPR, int VPL, bool ISMAX, int W, int RS, int NS>
+//
+// MODE 1/2 (fused gather, H8): the same agents, ring, keys and carries, but a
+// stage's rows are GATHERED: every lane cp.async-copies its 16-byte slices of
+// the rows x[src[e]] into the ring.  The src ids travel one ring cycle ahead:
+// issuing stage s also cp.async-loads the ids of stage s + NS into the same
+// buffer's id slots, so they have landed when stage s is consumed and its
+// buffer is refilled.  MODE 2 also stages w[e] and folds w[e] * x[src[e]].  An
+// out-of-range src id gathers a zero row (memory-safe; results for bad data
+// are unspecified).
+template <typename T, int VW, int LPR, int VPL, bool ISMAX, int W, int RS, int NS, int MODE = 0, bool SRC64 = false>
 __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const StreamParams p) {
     constexpr bool TMA = NS > 0;
+    static_assert(MODE == 0 || NS > 0, "the fused forms use the shared-memory ring");
     constexpr int NSX = TMA ? NS : 1;
     constexpr int G = 32 / LPR;
     using Cv = Conv<T, VW>;
@@ -101,6 +123,13 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
         reinterpret_cast<unsigned long long*>(smem_raw + (size_t)W * NS * stage_bytes) + warp * NS * G * RS;
     uint64_t* bars =
         reinterpret_cast<uint64_t*>(smem_raw + (size_t)W * NS * stage_bytes + (size_t)W * NS * G * RS * 8) + warp * NS;
+    float* wring = reinterpret_cast<float*>(smem_raw + (size_t)W * NS * stage_bytes + (size_t)W * NS * G * RS * 8 +
+                                            (size_t)W * NS * 8) +
+                   warp * NS * G * RS;
+    unsigned long long* sring =
+        reinterpret_cast<unsigned long long*>(smem_raw + (size_t)W * NS * stage_bytes + (size_t)W * NS * G * RS * 8 +
+                                              (size_t)W * NS * 8 + (MODE == 2 ? (size_t)W * NS * G * RS * 4 : 0)) +
+        warp * NS * G * RS;
 
     const long long seg_lo = p.seg_base, seg_hi = p.seg_base + p.S;
     const int F = p.F;
@@ -139,17 +168,64 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
         // int32 keys land in the low half of 8-byte slots: zero the ring once
         for (int i = lane; i < NS * G * RS; i += 32) wkey[i] = 0ull;
         if (lane == 0) {
-            for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1 + 32);  // producer + 32 cp.async arrivals
+            for (int s = 0; s < NS; ++s)
+                mbar_init(&bars[s], MODE == 0 ? 1 + 32 : 32);  // (TMA producer +) 32 cp.async arrivals
             fence_mbar_init();
         }
         __syncwarp();
     }
     const uint64_t pol = policy_evict_first();
 
+    const bool col_ok0 = li < p.NV;  // (fused forms: one 16-byte vector per lane)
+    // fused forms: the src ids of stage s + NS are cp.async-loaded into the id
+    // slot of buffer s % NS by issue(s) (so they land with stage s), and read
+    // back by the refill that issues stage s + NS (same lane, same slot)
+    auto id_copy = [&](int s) {  // src ids of stage s into the slots of buffer s % NS
+        const long long e = e_lo + (long long)s * RS + li;
+        if (li < RS && e < e_hi) {
+            void* dst = sring + ((s % NSX) * G + gi) * RS + li;
+            if (isz == 4)
+                cp_async_4(dst, static_cast<const unsigned char*>(p.src) + e * 4);
+            else
+                cp_async_8(dst, static_cast<const unsigned char*>(p.src) + e * 8);
+        }
+    };
+
     // all lanes: fill stage s of every group of the warp into buffer s % NS
-    auto issue = [&](int s) {
+    auto issue = [&](int s, long long sq) {
         const int b = s % NSX;
-        if (lane == 0) {
+        if constexpr (MODE >= 1) {
+            // gather: lane li copies its 16-byte slices of each of the stage's rows
+            // x[src] (cp.async, L2 only); the ids come from this buffer's id slots
+            long long c = e_hi - (e_lo + (long long)s * RS);
+            c = c < 0 ? 0 : (c > RS ? RS : c);
+            const unsigned long long* ids = sring + (b * G + gi) * RS;
+            const uint32_t gbase = smem_u32(wbuf) + (uint32_t)(b * stage_bytes + gi * RS * row_bytes + li * 16);
+            const T* xl = X + li * VW;  // this lane's 16-byte column of every row
+#pragma unroll
+            for (int r = 0; r < RS; ++r) {
+                if (r < c && col_ok0) {
+                    const unsigned long long raw = ids[r];  // broadcast within the group
+                    bool ok;
+                    const T* rowp;
+                    if constexpr (SRC64) {
+                        ok = raw < (unsigned long long)p.V;
+                        rowp = xl + (ok ? raw : 0ull) * (unsigned long long)F;
+                    } else {
+                        const unsigned sid = (unsigned)raw;
+                        ok = sid < (unsigned)p.V;  // V < 2^31 with int32 ids
+                        rowp = xl + (size_t)(ok ? sid : 0u) * (unsigned)F;
+                    }
+                    cp_async_16_zfill(gbase + (uint32_t)(r * row_bytes), rowp, ok ? 16u : 0u);
+                }
+            }
+            __syncwarp();  // every lane has read the id slots before they are refilled
+            id_copy(s + NSX);
+            if constexpr (MODE == 2) {
+                const long long e = e_lo + (long long)s * RS + li;
+                if (li < RS && e < e_hi) cp_async_4(wring + (b * G + gi) * RS + li, p.w + e);
+            }
+        } else if (lane == 0) {
             unsigned char* buf = wbuf + b * stage_bytes;
             uint32_t total = 0;
             int cnt[G];
@@ -177,8 +253,15 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
         }
         cp_async_mbar_arrive(&bars[b]);
     };
-    if constexpr (TMA)
-        for (int s = 0; s < NS && s < nst_w; ++s) issue(s);
+    if constexpr (MODE >= 1) {
+        // the ids of the first NS stages: loaded and waited for here (cp.async group)
+        for (int s = 0; s < NS && s < nst_w; ++s) id_copy(s);
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncwarp();
+        for (int s = 0; s < NS && s < nst_w; ++s) issue(s, 0);
+    } else if constexpr (TMA) {
+        for (int s = 0; s < NS && s < nst_w; ++s) issue(s, 0);
+    }
 
     const long long prevk = (e_lo > 0) ? load_index(p.idx, p.idx64, e_lo - 1) : KEY_BEFORE;
     const long long nextk = (e_hi < p.E) ? load_index(p.idx, p.idx64, e_hi) : KEY_AFTER;
@@ -247,7 +330,7 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
     // row of a sub-chunk); `heads` bit r = row r starts a segment; the key of
     // row r is held by lane (koff + r) of the group
     auto process = [&](const Raw (&rows)[SUB][VPL], unsigned heads, long long kmine, int koff, int cnt,
-                       long long r_base) {
+                       long long r_base, float wmine) {
 #pragma unroll
         for (int r = 0; r < SUB; ++r) {
             if (r >= cnt) break;
@@ -274,17 +357,23 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
 #pragma unroll
                     for (int q = 0; q < VW; ++q) acc[j][q] = identity<ISMAX>();
             }
+            float wr = 1.0f;
+            if constexpr (MODE == 2) wr = __shfl_sync(gmask, wmine, koff + r, LPR);
 #pragma unroll
             for (int j = 0; j < VPL; ++j) {
                 float f[VW];
                 Cv::unpack(raw[j], f);
 #pragma unroll
-                for (int q = 0; q < VW; ++q) acc[j][q] = fold<ISMAX>(acc[j][q], f[q]);
+                for (int q = 0; q < VW; ++q) acc[j][q] = fold<ISMAX>(acc[j][q], MODE == 2 ? wr * f[q] : f[q]);
             }
         }
     };
 
     if constexpr (TMA) {
+        // refill the buffer of stage s with stage s + NS (fused: src ids from the queue)
+        auto refill = [&](int s) {
+            if (s + NSX < nst_w) issue(s + NSX, 0);
+        };
         // 32-bit shared address of this lane's first vector in group gi's rows of buffer 0
         const uint32_t lane_s0 = smem_u32(wbuf) + gi * RS * row_bytes + li * VB;
 #pragma unroll 1
@@ -298,6 +387,8 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
             cnt = cnt < 0 ? 0 : (cnt > RS ? RS : cnt);
             const long long kmine = (li < cnt) ? gkey[li] : KEY_AFTER;
             const long long kprev = (li == 0) ? cur : ((li <= cnt) ? gkey[li - 1] : KEY_AFTER);
+            float wmine = 1.0f;
+            if constexpr (MODE == 2) wmine = (li < cnt) ? wring[(b * G + gi) * RS + li] : 0.0f;
             // is_seg of the whole stage (Alg. 1): row r starts a segment iff its
             // key differs from row r-1's (row -1: `cur`)
             const unsigned heads = __ballot_sync(gmask, li < cnt && kmine != kprev) >> (gi * LPR);
@@ -313,8 +404,8 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
                         rows[r][j] = (r < cnt && col_ok[j]) ? lds_vec<Raw>(sbase + r * row_bytes + j * LPR * VB) : Raw{};
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();
-                if (s + NSX < nst_w) issue(s + NSX);
-                process(rows, heads, kmine, 0, cnt, r_base);
+                refill(s);
+                process(rows, heads, kmine, 0, cnt, r_base, wmine);
             } else {
                 // large stages of small rows: SUB rows at a time, buffer released after
 #pragma unroll 1
@@ -327,11 +418,11 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
                             rows[r][j] = (r0 + r < cnt && col_ok[j])
                                              ? lds_vec<Raw>(sbase + (r0 + r) * row_bytes + j * LPR * VB)
                                              : Raw{};
-                    process(rows, heads >> r0, kmine, r0, cnt - r0, r_base + r0);
+                    process(rows, heads >> r0, kmine, r0, cnt - r0, r_base + r0, wmine);
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();
-                if (s + NSX < nst_w) issue(s + NSX);
+                refill(s);
             }
         }
     } else {
@@ -369,7 +460,7 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
             long long kprev = __shfl_up_sync(gmask, kmine, 1, LPR);
             if (li == 0) kprev = cur;
             const unsigned heads = __ballot_sync(gmask, li < cnt && kmine != kprev) >> (gi * LPR);
-            process(rows, heads, kmine, 0, cnt, r_base);
+            process(rows, heads, kmine, 0, cnt, r_base, 1.0f);
         }
     }
 

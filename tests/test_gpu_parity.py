@@ -274,6 +274,49 @@ def test_fused_bf16_and_weighted(geot, F):
     check(yw.cpu().numpy(), refw, "sum", "f32", "real")
 
 
+# -------------------------------------- fused gather through the stream kernel (H8)
+def fused_case(E, S, V, F, dtype, mode, kind, seed):
+    L = synth.stress_lengths(kind, E, S, seed)
+    dst = synth.lengths_to_index(L, "i64")
+    src = synth.src_index(seed + 1000, 0, E, V)
+    x = synth.values(seed, 0, V, F, dtype, mode)
+    return L, dst, src, x
+
+
+@pytest.mark.parametrize("F,dtype", [(32, "f32"), (64, "f32"), (128, "f32"), (64, "bf16"), (128, "bf16"),
+                                     (256, "bf16")])
+@pytest.mark.parametrize("op", ["sum", "mean", "max"])
+def test_fused_gather_stream(geot, F, dtype, op):
+    V, E, S = 20_000, 200_003, 15_000
+    tdt = torch.float32 if dtype == "f32" else torch.bfloat16
+    assert geot.geot_select_config(E, S, F, op, tdt, torch.int32, True).variant == 3
+    for mode in (("signed",) if op == "max" else ("int", "real")):
+        L, dst, src, x = fused_case(E, S, V, F, dtype, mode, "powerlaw15", F + 3)
+        ref = oracle.gather_segment_reduce(x, src, dst, S, op, nthreads=oracle.default_threads())
+        for it in (torch.int32, torch.int64):
+            y = geot.index_segment_reduce(torch.from_numpy(src).to(it).cuda(), torch.from_numpy(dst).to(it).cuda(),
+                                          to_torch_vals(x), op, num_segments=S)
+            check(from_torch_vals(y), ref, op, dtype, mode, counts=L, what=f"gather-stream F={F} {dtype} {op} {it}")
+
+
+@pytest.mark.parametrize("kind", synth.STRESS_KINDS)
+def test_fused_gather_stream_stress_and_weighted(geot, kind):
+    V, E, S, F = 9_000, 150_001, 12_000, 64
+    for op in ("sum", "mean", "max"):
+        L, dst, src, x = fused_case(E, S, V, F, "f32", "int", kind, 6)
+        ref = oracle.gather_segment_reduce(x, src, dst, S, op, nthreads=oracle.default_threads())
+        for cfg in ({"variant": 3}, {"variant": 1}):
+            y = geot.geot_gather_segment_reduce(torch.from_numpy(x).cuda(), torch.from_numpy(src).cuda(),
+                                                torch.from_numpy(dst).cuda(), S, op, cfg=cfg)
+            check(y.cpu().numpy(), ref, op, "f32", "int", counts=L, what=f"gather-stream {kind} {op} {cfg}")
+    w = synth.weights(2007, 0, E)
+    L, dst, src, x = fused_case(E, S, V, F, "f32", "real", kind, 7)
+    refw = oracle.gather_segment_reduce(x, src, dst, S, "sum", weight=w)
+    yw = geot.index_weight_segment_reduce(torch.from_numpy(src).cuda(), torch.from_numpy(dst).cuda(),
+                                          torch.from_numpy(w).cuda(), torch.from_numpy(x).cuda(), num_segments=S)
+    check(yw.cpu().numpy(), refw, "sum", "f32", "real", what=f"weighted gather-stream {kind}")
+
+
 # ---------------------------------------------------------------- integer kernels
 def test_offsets_partition_validate(geot):
     for kind in synth.STRESS_KINDS:

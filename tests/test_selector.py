@@ -77,7 +77,9 @@ def test_select_config_always_valid(L):
                         assert L.geot_select_config(nnz, S, F, 0, dt, 0, fused, ctypes.byref(c)) == 0
                         wide = 4 if dt == 0 else 8
                         if c.variant == 3:  # 16-byte lane vectors, 8/16/32 lanes per row
-                            assert not fused and c.vec_elems == wide and c.lanes_per_row >= 8
+                            assert c.vec_elems == wide and c.lanes_per_row >= 8
+                            assert not fused or (c.vecs_per_lane == 1 and (c.warps_per_cta, c.rows_per_group, c.stages)
+                                                 == (16, 6, 4))
                             assert F // wide <= c.lanes_per_row * c.vecs_per_lane
                             assert (c.warps_per_cta, c.rows_per_group, c.stages) in STREAM_PIPES[c.vecs_per_lane]
                         elif c.variant == 2:
