@@ -177,6 +177,9 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
     const uint64_t pol = policy_evict_first();
 
     const bool col_ok0 = li < p.NV;  // (fused forms: one 16-byte vector per lane)
+    const unsigned long long xrows = (unsigned long long)p.V;
+    const unsigned xrow_bytes = (unsigned)p.row_bytes;
+    const unsigned char* xlane = reinterpret_cast<const unsigned char*>(X) + li * 16;  // this lane's column
     // fused forms: the src ids of stage s + NS are cp.async-loaded into the id
     // slot of buffer s % NS by issue(s) (so they land with stage s), and read
     // back by the refill that issues stage s + NS (same lane, same slot)
@@ -197,26 +200,25 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
         if constexpr (MODE >= 1) {
             // gather: lane li copies its 16-byte slices of each of the stage's rows
             // x[src] (cp.async, L2 only); the ids come from this buffer's id slots
-            long long c = e_hi - (e_lo + (long long)s * RS);
-            c = c < 0 ? 0 : (c > RS ? RS : c);
+            long long cl = e_hi - (e_lo + (long long)s * RS);
+            const int c = cl < 0 ? 0 : (cl > RS ? RS : (int)cl);
             const unsigned long long* ids = sring + (b * G + gi) * RS;
             const uint32_t gbase = smem_u32(wbuf) + (uint32_t)(b * stage_bytes + gi * RS * row_bytes + li * 16);
-            const T* xl = X + li * VW;  // this lane's 16-byte column of every row
 #pragma unroll
             for (int r = 0; r < RS; ++r) {
                 if (r < c && col_ok0) {
                     const unsigned long long raw = ids[r];  // broadcast within the group
                     bool ok;
-                    const T* rowp;
+                    size_t off;  // byte offset of row src in x
                     if constexpr (SRC64) {
-                        ok = raw < (unsigned long long)p.V;
-                        rowp = xl + (ok ? raw : 0ull) * (unsigned long long)F;
+                        ok = raw < xrows;
+                        off = (size_t)(ok ? raw : 0ull) * xrow_bytes;
                     } else {
                         const unsigned sid = (unsigned)raw;
-                        ok = sid < (unsigned)p.V;  // V < 2^31 with int32 ids
-                        rowp = xl + (size_t)(ok ? sid : 0u) * (unsigned)F;
+                        ok = sid < (unsigned)xrows;  // V < 2^31 with int32 ids
+                        off = (size_t)(ok ? sid : 0u) * xrow_bytes;
                     }
-                    cp_async_16_zfill(gbase + (uint32_t)(r * row_bytes), rowp, ok ? 16u : 0u);
+                    cp_async_16_zfill(gbase + (uint32_t)(r * row_bytes), xlane + off, ok ? 16u : 0u);
                 }
             }
             __syncwarp();  // every lane has read the id slots before they are refilled
