@@ -24,7 +24,6 @@ import json
 import os
 import statistics
 import sys
-import threading
 import time
 
 import numpy as np
@@ -65,51 +64,67 @@ def peaks():
     return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+_SAMPLER_SRC = r"""
+import json, sys, threading, time
+import pynvml
+pynvml.nvmlInit()
+h = pynvml.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
+period = float(sys.argv[2])
+stop = threading.Event()
+threading.Thread(target=lambda: (sys.stdin.read(), stop.set()), daemon=True).start()
+samples, masks = [], 0
+print("ready", flush=True)
+while not stop.is_set():
+    try:
+        samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+        masks |= pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+    except Exception:
+        pass
+    time.sleep(period)
+print(json.dumps({"samples": samples, "mask": masks,
+                  "max": pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)}), flush=True)
+"""
+
+
 class ClockSampler:
-    """NVML sampling of SM clock and throttle reasons during the timed region."""
+    """NVML sampling of SM clock and throttle reasons during the timed region, in a
+    child process (the launch loop holds the GIL, which starved an in-process thread)."""
     REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
                0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
                0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
 
-    def __init__(self, index, period=0.002):
-        self.samples, self.reasons, self.max_mhz = [], set(), None
-        self.period, self._stop = period, threading.Event()
-        try:
-            import pynvml
-            pynvml.nvmlInit()
-            self.nv = pynvml
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
-        except Exception as e:  # pragma: no cover
-            self.nv, self.err = None, str(e)
-
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
-                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                for bit, name in self.REASONS.items():
-                    if r & bit and bit != 0x1:
-                        self.reasons.add(name)
-            except Exception:
-                pass
-            time.sleep(self.period)
+    def __init__(self, index, period=0.001):
+        self.index, self.period = index, period
+        self.samples, self.reasons, self.max_mhz, self.err = [], set(), None, ""
+        self.proc = None
 
     def __enter__(self):
-        if self.nv:
-            self._t = threading.Thread(target=self._run, daemon=True)
-            self._t.start()
+        import subprocess
+        try:
+            self.proc = subprocess.Popen([sys.executable, "-c", _SAMPLER_SRC, str(self.index), str(self.period)],
+                                         stdin=subprocess.PIPE, stdout=subprocess.PIPE, stderr=subprocess.PIPE,
+                                         text=True)
+            if self.proc.stdout.readline().strip() != "ready":
+                raise RuntimeError(self.proc.stderr.read()[-300:])
+        except Exception as e:  # pragma: no cover
+            self.err, self.proc = str(e), None
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        if self.nv:
-            self._t.join()
+        if not self.proc:
+            return
+        try:
+            out, _ = self.proc.communicate(input="", timeout=30)
+            d = json.loads(out.strip().splitlines()[-1])
+            self.samples, self.max_mhz = d["samples"], d["max"]
+            self.reasons = {name for bit, name in self.REASONS.items() if d["mask"] & bit and bit != 0x1}
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
 
     def summary(self):
-        if not self.nv:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": getattr(self, "err", "")}
-        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "error": self.err}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 

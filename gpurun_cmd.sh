@@ -1,3 +1,2 @@
-timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "fused or gather" 2>&1 | tail -2
-python tools/time_cfgs.py 114615892 232965 64 f32 powerlaw fused -- ''
-python tools/time_cfgs.py 16777216 1048576 32 f32 powerlaw fused -- ''
+bash tools/gpu_round.sh r1d
+timeout 900 python tools/report_configs.py --md gpurun_out/r1d_configs.md --jsonl gpurun_out/r1d_configs.jsonl > gpurun_out/r1d_configs.log 2>&1; echo "configs rc=$?"
