@@ -157,12 +157,17 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
     const int nrows = (int)(e_hi - e_lo);
     const int nst = (nrows + RS - 1) / RS;
     const int nst_w = __reduce_max_sync(0xffffffffu, nst);
+    const int nfull_w = __reduce_min_sync(0xffffffffu, nrows / RS);  // stages full in every group
     long long glo[G], ghi[G];  // every group's range, for the producer lane
 #pragma unroll
     for (int g = 0; g < G; ++g) {
         glo[g] = __shfl_sync(0xffffffffu, e_lo, g * LPR);
         ghi[g] = __shfl_sync(0xffffffffu, e_hi, g * LPR);
     }
+
+    const unsigned char* xg[G];  // first row of every group's range (bytes)
+#pragma unroll
+    for (int g = 0; g < G; ++g) xg[g] = reinterpret_cast<const unsigned char*>(X) + glo[g] * (long long)row_bytes;
 
     if constexpr (TMA) {
         // int32 keys land in the low half of 8-byte slots: zero the ring once
@@ -227,6 +232,14 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
                 const long long e = e_lo + (long long)s * RS + li;
                 if (li < RS && e < e_hi) cp_async_4(wring + (b * G + gi) * RS + li, p.w + e);
             }
+        } else if (lane == 0 && s < nfull_w) {
+            // every group has RS rows in this stage (all but the last stage or two)
+            unsigned char* buf = wbuf + b * stage_bytes;
+            const uint32_t gb = (uint32_t)(RS * row_bytes);
+            mbar_arrive_expect_tx(&bars[b], G * gb);
+            const size_t soff = (size_t)s * gb;
+#pragma unroll
+            for (int g = 0; g < G; ++g) bulk_g2s(buf + g * gb, xg[g] + soff, gb, &bars[b], pol);
         } else if (lane == 0) {
             unsigned char* buf = wbuf + b * stage_bytes;
             uint32_t total = 0;
@@ -366,7 +379,20 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
                 float f[VW];
                 Cv::unpack(raw[j], f);
 #pragma unroll
-                for (int q = 0; q < VW; ++q) acc[j][q] = fold<ISMAX>(acc[j][q], MODE == 2 ? wr * f[q] : f[q]);
+                for (int q = 0; q < VW; ++q)
+                    if constexpr (MODE == 2) f[q] = wr * f[q];
+                if constexpr (!ISMAX && VW % 2 == 0) {
+                    // packed fp32x2 adds (sm_100 FADD2): two IEEE RN adds per instruction
+#pragma unroll
+                    for (int q = 0; q < VW; q += 2) {
+                        const float2 t = __fadd2_rn(make_float2(acc[j][q], acc[j][q + 1]), make_float2(f[q], f[q + 1]));
+                        acc[j][q] = t.x;
+                        acc[j][q + 1] = t.y;
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < VW; ++q) acc[j][q] = fold<ISMAX>(acc[j][q], f[q]);
+                }
             }
         }
     };

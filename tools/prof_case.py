@@ -1,4 +1,5 @@
-"""Run one configuration a few times (for ncu):  python tools/prof_case.py E S F dtype dist [cfg-json] [fused]"""
+"""Run one configuration a few times (for ncu):
+python tools/prof_case.py E S F dtype dist [cfg-json|-] [fused|-] [op] [mode]"""
 import json
 import os
 import sys
@@ -14,16 +15,18 @@ E, S, F = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3])
 dt, dist = sys.argv[4], sys.argv[5]
 cfg = json.loads(sys.argv[6]) if len(sys.argv) > 6 and sys.argv[6] not in ("", "-") else None
 fused = len(sys.argv) > 7 and sys.argv[7] == "fused"
+op = sys.argv[8] if len(sys.argv) > 8 else "sum"
+mode = sys.argv[9] if len(sys.argv) > 9 else ("signed" if op == "max" else "real")
 tdt = torch.float32 if dt == "f32" else torch.bfloat16
 L = synth.segment_lengths(E, S, dist, 5)
 idx = sd.index_from_lengths(L)
 if fused:
-    x = sd.values(S, F, 5, dtype=tdt)
+    x = sd.values(S, F, 5, dtype=tdt, mode=mode)
     src = sd.src_index(E, S, 1005)
-    run = lambda: geot.geot_gather_segment_reduce(x, src, idx, S, "sum", cfg=cfg)  # noqa: E731
+    run = lambda: geot.geot_gather_segment_reduce(x, src, idx, S, op, cfg=cfg)  # noqa: E731
 else:
-    X = sd.values(E, F, 5, dtype=tdt)
-    run = lambda: geot.geot_segment_reduce(X, idx, S, "sum", cfg=cfg)  # noqa: E731
+    X = sd.values(E, F, 5, dtype=tdt, mode=mode)
+    run = lambda: geot.geot_segment_reduce(X, idx, S, op, cfg=cfg)  # noqa: E731
 for _ in range(6):
     run()
 torch.cuda.synchronize()
