@@ -237,9 +237,19 @@ __global__ void __launch_bounds__(256) edge_tile_kernel(const EdgeTileParams p) 
                         float f[VW];
                         Cv::unpack(r[j], f);
 #pragma unroll
-                        for (int q = 0; q < VW; ++q) {
-                            const float x = (MODE == 2) ? wt * f[q] : f[q];
-                            acc[j][q] = fold<ISMAX>(acc[j][q], x);
+                        for (int q = 0; q < VW; ++q)
+                            if constexpr (MODE == 2) f[q] = wt * f[q];
+                        if constexpr (!ISMAX && VW % 2 == 0) {  // packed fp32x2 adds (FADD2)
+#pragma unroll
+                            for (int q = 0; q < VW; q += 2) {
+                                const float2 t =
+                                    __fadd2_rn(make_float2(acc[j][q], acc[j][q + 1]), make_float2(f[q], f[q + 1]));
+                                acc[j][q] = t.x;
+                                acc[j][q + 1] = t.y;
+                            }
+                        } else {
+#pragma unroll
+                            for (int q = 0; q < VW; ++q) acc[j][q] = fold<ISMAX>(acc[j][q], f[q]);
                         }
                     }
                 }

@@ -354,8 +354,18 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, 2)
 #pragma unroll
         for (int i = 1; i < ITEMS; ++i) {
             const bool h = (hm >> i) & 1u;
+            if constexpr (OP != OP_MAX && F % 2 == 0) {  // packed fp32x2 adds (FADD2)
 #pragma unroll
-            for (int f = 0; f < F; ++f) acc[i][f] = h ? acc[i][f] : nfold<OP>(acc[i - 1][f], acc[i][f]);
+                for (int f = 0; f < F; f += 2) {
+                    const float2 t = __fadd2_rn(make_float2(acc[i - 1][f], acc[i - 1][f + 1]),
+                                                make_float2(acc[i][f], acc[i][f + 1]));
+                    acc[i][f] = h ? acc[i][f] : t.x;
+                    acc[i][f + 1] = h ? acc[i][f + 1] : t.y;
+                }
+            } else {
+#pragma unroll
+                for (int f = 0; f < F; ++f) acc[i][f] = h ? acc[i][f] : nfold<OP>(acc[i - 1][f], acc[i][f]);
+            }
         }
         const KT klast = k[ITEMS - 1];  // padded: the last valid key
         const bool last_ends = nv > 0 && klast != kn;
