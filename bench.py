@@ -93,7 +93,7 @@ class ClockSampler:
                0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
                0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
 
-    def __init__(self, index, period=0.001):
+    def __init__(self, index, period=float(os.environ.get("GEOT_CLOCK_PERIOD", "0.005"))):
         self.index, self.period = index, period
         self.samples, self.reasons, self.max_mhz, self.err = [], set(), None, ""
         self.proc = None

@@ -182,6 +182,26 @@ geot_status geot_segment_reduce_ex(const void* src, const void* idx, int64_t nnz
                                    geot_itype itype, void* out, void* workspace, size_t ws_bytes,
                                    const geot_config* cfg, cudaStream_t stream);
 
+/* f4 (SURVEY §8(e), §8(f) "output all-gather fused into the epilogue"): the
+ * H9 shard form of geot_segment_reduce_ex whose finished rows are stored
+ * straight into EVERY rank's replica of the full output, so no separate
+ * all-gather collective follows.
+ *   outs     host array of nouts (1..8) device pointers, each a
+ *            [total_segments, F] (dtype) buffer reachable from this GPU: its
+ *            own replica and the peers' replicas mapped into this process
+ *            (cudaDeviceEnablePeerAccess, CUDA IPC or symmetric memory); the
+ *            stores to a peer travel over NVLink.
+ *   rows [seg_base, seg_base + num_segments) of every replica are written
+ *   (empty segments zero-filled); no other row is touched.  Ownership,
+ *   workspace, stream and error behaviour as geot_segment_reduce_ex; nouts
+ *   outside 1..8 or a NULL pointer -> GEOT_ERR_INVALID_VALUE.  Stream-ordered
+ *   on THIS GPU only: the caller orders the peers' reads after it (e.g. a
+ *   barrier after synchronising the stream). */
+geot_status geot_segment_reduce_allgather(const void* src, const void* idx, int64_t nnz, int64_t seg_base,
+                                          int64_t num_segments, int64_t F, geot_reduce op, geot_dtype dtype,
+                                          geot_itype itype, void* const* outs, int nouts, void* workspace,
+                                          size_t ws_bytes, const geot_config* cfg, cudaStream_t stream);
+
 /* H8: fused gather + segment reduction (P:293 index_segment_reduce):
  *   Y[s,:] = f over { x[src_idx[e], :] : dst_idx[e] == s }.
  *   x        [num_x_rows, F] node features (dtype), device

@@ -124,6 +124,33 @@ def geot_workspace_size(nnz, num_segments, F, op="sum", dtype=torch.float32, ity
                                       _cfgp(cfg)))
 
 
+def geot_segment_reduce_allgather(src, idx, seg_base, num_segments, outs, op="sum", cfg=None):
+    """f4: reduce this shard (segments [seg_base, seg_base + num_segments)) and store every
+    finished row into each replica in `outs` (full [total_segments, F] buffers; peer replicas
+    must be mapped into this process, e.g. by shard.open_peer_replicas).  Fused all-gather
+    epilogue: no collective follows; order peer reads after this call (stream sync + barrier)."""
+    dev = _dev(src, idx)
+    if src.dim() != 2 or idx.dim() != 1 or src.shape[0] != idx.shape[0]:
+        raise ValueError("src must be [nnz, F] and idx [nnz]")
+    E, F = src.shape
+    if not 1 <= len(outs) <= 8:
+        raise ValueError("1..8 output replicas")
+    for o in outs:
+        if o.dim() != 2 or o.shape[1] != F or o.dtype != src.dtype or o.shape[0] < seg_base + num_segments:
+            raise ValueError("every replica must be [total_segments, F] with src's dtype")
+        if not o.is_contiguous():
+            raise ValueError("replicas must be contiguous")
+    ptrs = (ctypes.c_void_p * len(outs))(*[o.data_ptr() for o in outs])
+    ws_n = _L.geot_workspace_size(E, num_segments, F, _op(op), _dt(src), _it(idx), 0, _cfgp(cfg))
+    ws, ws_bytes = _workspace(dev, ws_n)
+    with torch.cuda.device(dev):
+        st = _L.geot_segment_reduce_allgather(_ptr(src), _ptr(idx), E, seg_base, num_segments, F, _op(op), _dt(src),
+                                              _it(idx), ptrs, len(outs), _ptr(ws), ws_bytes, _cfgp(cfg),
+                                              _stream(dev))
+    _lib.check(st, "geot_segment_reduce_allgather")
+    return outs
+
+
 def _num_segments(idx, num_segments):
     if num_segments is not None:
         return int(num_segments)

@@ -59,6 +59,8 @@ SIGNATURES = {
     "geot_segment_reduce": ([_vp, _vp, _i64, _i64, _i64, _i32, _i32, _i32, _vp, _vp, _sz, _vp], _i32),
     "geot_segment_reduce_ex": ([_vp, _vp, _i64, _i64, _i64, _i64, _i32, _i32, _i32, _vp, _vp, _sz, _cfgp, _vp],
                                _i32),
+    "geot_segment_reduce_allgather": ([_vp, _vp, _i64, _i64, _i64, _i64, _i32, _i32, _i32, ctypes.POINTER(_vp), _i32,
+                                       _vp, _sz, _cfgp, _vp], _i32),
     "geot_gather_segment_reduce": ([_vp, _i64, _vp, _vp, _i64, _i64, _i64, _i32, _i32, _i32, _vp, _vp, _sz, _vp],
                                    _i32),
     "geot_gather_weight_segment_reduce": ([_vp, _i64, _vp, _vp, _vp, _i64, _i64, _i64, _i32, _i32, _vp, _vp, _sz,

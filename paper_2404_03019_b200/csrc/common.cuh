@@ -271,6 +271,18 @@ __device__ __forceinline__ uint16_t lds_vec<uint16_t>(uint32_t addr) {
     return r;
 }
 
+// Output destinations (f4, fused all-gather epilogue): every finished row
+// `key` is stored to ptr[q] + (key - row_off) * F for q < n.  A plain call has
+// n = 1, ptr[0] = out, row_off = seg_base; the all-gather form has one full
+// [S_total, F] buffer per rank (peer / IPC-mapped pointers reached over
+// NVLink) and row_off = 0, so each rank writes its rows into every replica.
+constexpr int kMaxOuts = 8;
+struct OutSet {
+    void* ptr[kMaxOuts];
+    int n;
+    long long row_off;
+};
+
 // Per-tile carry metadata written by the reduction kernel on EVERY call (so
 // the workspace needs no initialisation) and read by the fix-up kernel.
 struct TileMeta {
@@ -287,7 +299,8 @@ struct EdgeTileParams {
     const void* idx;     // [E] sorted segment ids
     const void* src;     // [E] gather rows (fused), else null
     const float* w;      // [E] weights (weighted fused), else null
-    void* out;           // [S, F]
+    void* out;           // [S, F]  (== outs.ptr[0])
+    OutSet outs;         // every destination of a finished row
     float* carry_h;      // [ntiles, F] tile-head partials
     float* carry_t;      // [ntiles, F] tile-tail partials
     TileMeta* meta;      // [ntiles]

@@ -80,22 +80,23 @@ __global__ void __launch_bounds__(256) edge_tile_kernel(const EdgeTileParams p) 
     const long long seg_lo = p.seg_base, seg_hi = p.seg_base + p.S;  // valid keys [lo, hi)
     const int F = p.F;
     const T* __restrict__ X = static_cast<const T*>(p.X);
-    T* __restrict__ out = static_cast<T*>(p.out);
 
     auto vec_col = [&](int j) { return fv0 + li + j * LPR; };
 
     // exactly-once store of a finished segment row (H7 epilogue)
     auto write_row = [&](long long key, const float (&acc)[VPL][VW], long long count) {
         if (key < seg_lo || key >= seg_hi) return;
-        T* rowp = out + (key - seg_lo) * (long long)F;
+        for (int d = 0; d < p.outs.n; ++d) {
+            T* rowp = static_cast<T*>(p.outs.ptr[d]) + (key - p.outs.row_off) * (long long)F;
 #pragma unroll
-        for (int j = 0; j < VPL; ++j) {
-            const int v = vec_col(j);
-            if (v < p.NV) {
-                float o[VW];
+            for (int j = 0; j < VPL; ++j) {
+                const int v = vec_col(j);
+                if (v < p.NV) {
+                    float o[VW];
 #pragma unroll
-                for (int q = 0; q < VW; ++q) o[q] = finalize(acc[j][q], p.op, count);
-                st_vec(reinterpret_cast<Raw*>(rowp + (long long)v * VW), Cv::pack(o));
+                    for (int q = 0; q < VW; ++q) o[q] = finalize(acc[j][q], p.op, count);
+                    st_vec(reinterpret_cast<Raw*>(rowp + (long long)v * VW), Cv::pack(o));
+                }
             }
         }
     };
@@ -107,14 +108,15 @@ __global__ void __launch_bounds__(256) edge_tile_kernel(const EdgeTileParams p) 
 #pragma unroll
         for (int q = 0; q < VW; ++q) z[q] = 0.0f;
         const Raw zr = Cv::pack(z);
-        for (long long r = r0; r < r1; ++r) {
-            T* rowp = out + (r - seg_lo) * (long long)F;
+        for (int d = 0; d < p.outs.n; ++d)
+            for (long long r = r0; r < r1; ++r) {
+                T* rowp = static_cast<T*>(p.outs.ptr[d]) + (r - p.outs.row_off) * (long long)F;
 #pragma unroll
-            for (int j = 0; j < VPL; ++j) {
-                const int v = vec_col(j);
-                if (v < p.NV) st_vec(reinterpret_cast<Raw*>(rowp + (long long)v * VW), zr);
+                for (int j = 0; j < VPL; ++j) {
+                    const int v = vec_col(j);
+                    if (v < p.NV) st_vec(reinterpret_cast<Raw*>(rowp + (long long)v * VW), zr);
+                }
             }
-        }
     };
     auto slot_store = [&](float* base, int grp, const float (&acc)[VPL][VW]) {
 #pragma unroll
@@ -373,7 +375,6 @@ __global__ void __launch_bounds__(256) carry_fixup_kernel(const EdgeTileParams p
     const long long key = m.head_key;
     if (key < p.seg_base || key >= p.seg_base + p.S) return;
     const long long count = m.head_end - mu.tail_start;
-    T* orow = static_cast<T*>(p.out) + (key - p.seg_base) * (long long)p.F;
     for (int f = lane; f < p.F; f += 32) {
         double acc = (double)p.carry_t[u * (long long)p.F + f];
         for (long long v = u + 1; v <= t; ++v) {
@@ -382,10 +383,13 @@ __global__ void __launch_bounds__(256) carry_fixup_kernel(const EdgeTileParams p
         }
         float r = (float)acc;
         r = finalize(r, p.op, count);
-        if constexpr (sizeof(T) == 4)
-            reinterpret_cast<float*>(orow)[f] = r;
-        else
-            reinterpret_cast<uint16_t*>(orow)[f] = f2bf_bits(r);
+        for (int d = 0; d < p.outs.n; ++d) {
+            T* orow = static_cast<T*>(p.outs.ptr[d]) + (key - p.outs.row_off) * (long long)p.F;
+            if constexpr (sizeof(T) == 4)
+                reinterpret_cast<float*>(orow)[f] = r;
+            else
+                reinterpret_cast<uint16_t*>(orow)[f] = f2bf_bits(r);
+        }
     }
 }
 

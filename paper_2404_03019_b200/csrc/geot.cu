@@ -226,31 +226,46 @@ static edge_launcher pick_launcher(geot_dtype dt, int mode) {
 }
 
 // The shared body of every reduction entry point.
+static OutSet single_out(void* out, long long seg_base) {
+    OutSet os{};
+    os.ptr[0] = out;
+    os.n = 1;
+    os.row_off = seg_base;
+    return os;
+}
+
 static geot_status reduce_common(const void* X, long long V, const void* src_idx, const void* idx, const float* w,
                                  long long nnz, long long seg_base, long long S, long long F, geot_reduce op,
-                                 geot_dtype dt, geot_itype it, void* out, void* ws, size_t ws_bytes,
+                                 geot_dtype dt, geot_itype it, const OutSet& os, void* ws, size_t ws_bytes,
                                  const geot_config* user_cfg, cudaStream_t stream, int mode) {
+    void* out = os.ptr[0];
     geot_status st = check_enums(op, dt, it);
     if (st != GEOT_OK) return st;
     if (nnz < 0 || S < 0 || F < 1 || V < 0) return GEOT_ERR_INVALID_VALUE;
     if (F > (1LL << 30) || nnz > (1LL << 47)) return GEOT_ERR_UNSUPPORTED;
     if (mode == 2 && op != GEOT_SUM) return GEOT_ERR_UNSUPPORTED;
     if (S == 0) return GEOT_OK;
-    if (!out) return GEOT_ERR_INVALID_VALUE;
+    for (int d = 0; d < os.n; ++d)
+        if (!os.ptr[d]) return GEOT_ERR_INVALID_VALUE;
     if (nnz > 0 && (!X || !idx || (mode >= 1 && !src_idx) || (mode == 2 && !w))) return GEOT_ERR_INVALID_VALUE;
     const size_t esz = dt == GEOT_F32 ? 4 : 2;
     if (nnz == 0) {  // every segment is empty
         const long long bytes = S * F * (long long)esz;
         const int blocks = (int)std::min<long long>((bytes / 16 + 255) / 256 + 1, (long long)sm_count() * 8);
-        zero_fill_kernel<<<blocks, 256, 0, stream>>>(static_cast<unsigned char*>(out), bytes);
-        g_launches.fetch_add(1, std::memory_order_relaxed);
+        for (int d = 0; d < os.n; ++d) {
+            unsigned char* o = static_cast<unsigned char*>(os.ptr[d]) + (seg_base - os.row_off) * F * (long long)esz;
+            zero_fill_kernel<<<blocks, 256, 0, stream>>>(o, bytes);
+            g_launches.fetch_add(1, std::memory_order_relaxed);
+        }
         return from_cuda(cudaGetLastError());
     }
     geot_config c;
     st = resolve_config(nnz, S, F, op, dt, it, mode >= 1, user_cfg, &c);
     if (st != GEOT_OK) return st;
     // vector path needs 16-byte aligned row starts of the value/output arrays
-    if ((c.vec_elems > 1 || c.variant == GEOT_VARIANT_STREAM) && !(aligned(X, 16) && aligned(out, 16))) {
+    bool outs_aligned = true;
+    for (int d = 0; d < os.n; ++d) outs_aligned = outs_aligned && aligned(os.ptr[d], 16);
+    if ((c.vec_elems > 1 || c.variant == GEOT_VARIANT_STREAM) && !(aligned(X, 16) && outs_aligned)) {
         if (user_cfg && (user_cfg->vec_elems > 1 || user_cfg->variant == GEOT_VARIANT_STREAM))
             return GEOT_ERR_UNSUPPORTED;
         c.variant = GEOT_VARIANT_EDGE_TILE;
@@ -270,6 +285,7 @@ static geot_status reduce_common(const void* X, long long V, const void* src_idx
             np.X = X;
             np.idx = idx;
             np.out = out;
+            np.outs = os;
             np.carry_h = reinterpret_cast<float*>(wsb + L.carry_h);
             np.carry_t = reinterpret_cast<float*>(wsb + L.carry_t);
             np.meta = reinterpret_cast<TileMeta*>(wsb + L.meta);
@@ -300,6 +316,7 @@ static geot_status reduce_common(const void* X, long long V, const void* src_idx
             sp.X = X;
             sp.idx = idx;
             sp.out = out;
+            sp.outs = os;
             sp.meta = L.total ? reinterpret_cast<TileMeta*>(wsb + L.meta) : nullptr;
             sp.carry_h = L.total ? reinterpret_cast<float*>(wsb + L.carry_h) : nullptr;
             sp.carry_t = L.total ? reinterpret_cast<float*>(wsb + L.carry_t) : nullptr;
@@ -321,6 +338,7 @@ static geot_status reduce_common(const void* X, long long V, const void* src_idx
             sp.V = V;
             EdgeTileParams fx{};
             fx.out = out;
+            fx.outs = os;
             fx.meta = sp.meta;
             fx.carry_h = sp.carry_h;
             fx.carry_t = sp.carry_t;
@@ -365,6 +383,7 @@ static geot_status reduce_common(const void* X, long long V, const void* src_idx
     p.src = src_idx;
     p.w = w;
     p.out = out;
+    p.outs = os;
     p.meta = L.total ? reinterpret_cast<TileMeta*>(wsb + L.meta) : nullptr;
     p.carry_h = L.total ? reinterpret_cast<float*>(wsb + L.carry_h) : nullptr;
     p.carry_t = L.total ? reinterpret_cast<float*>(wsb + L.carry_t) : nullptr;
@@ -473,24 +492,24 @@ geot_status geot_workspace_init(void* workspace, size_t ws_bytes, cudaStream_t s
 geot_status geot_segment_reduce(const void* src, const void* idx, int64_t nnz, int64_t num_segments, int64_t F,
                                 geot_reduce op, geot_dtype dtype, geot_itype itype, void* out, void* workspace,
                                 size_t ws_bytes, cudaStream_t stream) {
-    return reduce_common(src, nnz, nullptr, idx, nullptr, nnz, 0, num_segments, F, op, dtype, itype, out, workspace,
-                         ws_bytes, nullptr, stream, 0);
+    return reduce_common(src, nnz, nullptr, idx, nullptr, nnz, 0, num_segments, F, op, dtype, itype,
+                         single_out(out, 0), workspace, ws_bytes, nullptr, stream, 0);
 }
 
 geot_status geot_segment_reduce_ex(const void* src, const void* idx, int64_t nnz, int64_t seg_base,
                                    int64_t num_segments, int64_t F, geot_reduce op, geot_dtype dtype,
                                    geot_itype itype, void* out, void* workspace, size_t ws_bytes,
                                    const geot_config* cfg, cudaStream_t stream) {
-    return reduce_common(src, nnz, nullptr, idx, nullptr, nnz, seg_base, num_segments, F, op, dtype, itype, out,
-                         workspace, ws_bytes, cfg, stream, 0);
+    return reduce_common(src, nnz, nullptr, idx, nullptr, nnz, seg_base, num_segments, F, op, dtype, itype,
+                         single_out(out, seg_base), workspace, ws_bytes, cfg, stream, 0);
 }
 
 geot_status geot_gather_segment_reduce(const void* x, int64_t num_x_rows, const void* src_idx, const void* dst_idx,
                                        int64_t nnz, int64_t num_segments, int64_t F, geot_reduce op,
                                        geot_dtype dtype, geot_itype itype, void* out, void* workspace,
                                        size_t ws_bytes, cudaStream_t stream) {
-    return reduce_common(x, num_x_rows, src_idx, dst_idx, nullptr, nnz, 0, num_segments, F, op, dtype, itype, out,
-                         workspace, ws_bytes, nullptr, stream, 1);
+    return reduce_common(x, num_x_rows, src_idx, dst_idx, nullptr, nnz, 0, num_segments, F, op, dtype, itype,
+                         single_out(out, 0), workspace, ws_bytes, nullptr, stream, 1);
 }
 
 geot_status geot_gather_weight_segment_reduce(const void* x, int64_t num_x_rows, const void* src_idx,
@@ -498,7 +517,7 @@ geot_status geot_gather_weight_segment_reduce(const void* x, int64_t num_x_rows,
                                               int64_t num_segments, int64_t F, geot_dtype dtype, geot_itype itype,
                                               void* out, void* workspace, size_t ws_bytes, cudaStream_t stream) {
     return reduce_common(x, num_x_rows, src_idx, dst_idx, weight, nnz, 0, num_segments, F, GEOT_SUM, dtype, itype,
-                         out, workspace, ws_bytes, nullptr, stream, 2);
+                         single_out(out, 0), workspace, ws_bytes, nullptr, stream, 2);
 }
 
 geot_status geot_gather_segment_reduce_ex(const void* x, int64_t num_x_rows, const void* src_idx,
@@ -507,7 +526,20 @@ geot_status geot_gather_segment_reduce_ex(const void* x, int64_t num_x_rows, con
                                           geot_itype itype, void* out, void* workspace, size_t ws_bytes,
                                           const geot_config* cfg, cudaStream_t stream) {
     return reduce_common(x, num_x_rows, src_idx, dst_idx, weight, nnz, seg_base, num_segments, F, op, dtype, itype,
-                         out, workspace, ws_bytes, cfg, stream, weight ? 2 : 1);
+                         single_out(out, seg_base), workspace, ws_bytes, cfg, stream, weight ? 2 : 1);
+}
+
+geot_status geot_segment_reduce_allgather(const void* src, const void* idx, int64_t nnz, int64_t seg_base,
+                                          int64_t num_segments, int64_t F, geot_reduce op, geot_dtype dtype,
+                                          geot_itype itype, void* const* outs, int nouts, void* workspace,
+                                          size_t ws_bytes, const geot_config* cfg, cudaStream_t stream) {
+    if (!outs || nouts < 1 || nouts > kMaxOuts || seg_base < 0) return GEOT_ERR_INVALID_VALUE;
+    OutSet os{};
+    for (int d = 0; d < nouts; ++d) os.ptr[d] = outs[d];
+    os.n = nouts;
+    os.row_off = 0;  // every replica holds the full output: rows are global segment ids
+    return reduce_common(src, nnz, nullptr, idx, nullptr, nnz, seg_base, num_segments, F, op, dtype, itype, os,
+                         workspace, ws_bytes, cfg, stream, 0);
 }
 
 geot_status geot_segment_reduce_backward(const void* grad_out, const void* idx, int64_t nnz, int64_t num_segments,

@@ -42,7 +42,8 @@ namespace geot {
 struct NarrowParams {
     const void* X;
     const void* idx;
-    void* out;
+    void* out;      // == outs.ptr[0]
+    OutSet outs;    // every destination of a finished row (f4)
     float* carry_h;
     float* carry_t;
     TileMeta* meta;
@@ -197,8 +198,8 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, 2)
 
     const T* __restrict__ X = static_cast<const T*>(p.X);
     const KT* __restrict__ I = static_cast<const KT*>(p.idx);
-    T* __restrict__ out = static_cast<T*>(p.out);
     const long long seg_lo = p.seg_base, seg_hi = p.seg_base + p.S;
+    T* __restrict__ out0 = static_cast<T*>(p.outs.ptr[0]) + (seg_lo - p.outs.row_off) * F;  // row of key seg_lo
     const long long E = p.E;
 
     __shared__ unsigned s_ticket;
@@ -245,7 +246,8 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, 2)
         float z[F];
 #pragma unroll
         for (int f = 0; f < F; ++f) z[f] = 0.0f;
-        for (long long r = r0; r < r1; ++r) st_row<T, F>(out + (r - seg_lo) * F, z);
+        for (int d = 0; d < p.outs.n; ++d)
+            for (long long r = r0; r < r1; ++r) st_row<T, F>(static_cast<T*>(p.outs.ptr[d]) + (r - p.outs.row_off) * F, z);
     };
     // a store at key k (32-bit relative arithmetic for int32 keys; memory-safe)
     const KT kseg_lo = (KT)seg_lo;
@@ -264,7 +266,11 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, 2)
         float o[F];
 #pragma unroll
         for (int f = 0; f < F; ++f) o[f] = (OP == OP_MEAN) ? __fdiv_rn(v[f], (float)count) : v[f];
-        if (ok) st_row<T, F>(out + rel * F, o);
+        if (ok) {
+            st_row<T, F>(out0 + rel * F, o);
+            for (int d = 1; d < p.outs.n; ++d)  // replicas (f4): global row index
+                st_row<T, F>(static_cast<T*>(p.outs.ptr[d]) + ((long long)rel + seg_lo - p.outs.row_off) * F, o);
+        }
     };
 
     const bool active = e_lo < e_hi;

@@ -53,7 +53,8 @@ struct StreamCtrl {
 struct StreamParams {
     const void* X;
     const void* idx;
-    void* out;
+    void* out;        // == outs.ptr[0]
+    OutSet outs;      // every destination of a finished row (f4)
     float* carry_h;   // [NA, F] partial of an agent lying wholly inside one segment
     float* carry_t;   // [NA, F] tail partial of a segment continuing past the agent
     TileMeta* meta;   // [NA] flags / tail_start of publishing agents
@@ -134,7 +135,8 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
     const long long seg_lo = p.seg_base, seg_hi = p.seg_base + p.S;
     const int F = p.F;
     const T* __restrict__ X = static_cast<const T*>(p.X);
-    T* __restrict__ out = static_cast<T*>(p.out);
+    // destination 0 addressed by key - seg_lo (row of key seg_lo); replicas (f4) below
+    T* __restrict__ out = static_cast<T*>(p.outs.ptr[0]) + (seg_lo - p.outs.row_off) * (long long)F;
     const int isz = p.idx64 ? 8 : 4;
     const unsigned char* idxb = static_cast<const unsigned char*>(p.idx);
 
@@ -285,16 +287,25 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
     auto vec_col = [&](int j) { return li + j * LPR; };
     auto write_row = [&](long long key, const float (&acc)[VPL][VW], long long count) {
         if (key < seg_lo || key >= seg_hi) return;
-        T* rowp = out + (key - seg_lo) * (long long)F;
+        Raw packed[VPL];
 #pragma unroll
         for (int j = 0; j < VPL; ++j) {
-            const int v = vec_col(j);
-            if (v < p.NV) {
-                float o[VW];
+            float o[VW];
 #pragma unroll
-                for (int q = 0; q < VW; ++q) o[q] = finalize(acc[j][q], p.op, count);
-                st_vec(reinterpret_cast<Raw*>(rowp + v * VW), Cv::pack(o));
-            }
+            for (int q = 0; q < VW; ++q) o[q] = finalize(acc[j][q], p.op, count);
+            packed[j] = Cv::pack(o);
+        }
+        {
+            T* rowp = out + (key - seg_lo) * (long long)F;
+#pragma unroll
+            for (int j = 0; j < VPL; ++j)
+                if (vec_col(j) < p.NV) st_vec(reinterpret_cast<Raw*>(rowp + vec_col(j) * VW), packed[j]);
+        }
+        for (int d = 1; d < p.outs.n; ++d) {  // replicas (f4)
+            T* rowp = static_cast<T*>(p.outs.ptr[d]) + (key - p.outs.row_off) * (long long)F;
+#pragma unroll
+            for (int j = 0; j < VPL; ++j)
+                if (vec_col(j) < p.NV) st_vec(reinterpret_cast<Raw*>(rowp + vec_col(j) * VW), packed[j]);
         }
     };
     auto gap_fill = [&](long long lo_k, long long hi_k) {
@@ -304,14 +315,16 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
 #pragma unroll
         for (int q = 0; q < VW; ++q) z[q] = 0.0f;
         const Raw zr = Cv::pack(z);
-        for (long long r = r0; r < r1; ++r) {
-            T* rowp = out + (r - seg_lo) * (long long)F;
+        for (int d = 0; d < p.outs.n; ++d)
+            for (long long r = r0; r < r1; ++r) {
+                T* rowp = (d == 0 ? out + (r - seg_lo) * (long long)F
+                                  : static_cast<T*>(p.outs.ptr[d]) + (r - p.outs.row_off) * (long long)F);
 #pragma unroll
-            for (int j = 0; j < VPL; ++j) {
-                const int v = vec_col(j);
-                if (v < p.NV) st_vec(reinterpret_cast<Raw*>(rowp + v * VW), zr);
+                for (int j = 0; j < VPL; ++j) {
+                    const int v = vec_col(j);
+                    if (v < p.NV) st_vec(reinterpret_cast<Raw*>(rowp + v * VW), zr);
+                }
             }
-        }
     };
     auto carry_store = [&](float* carry, const float (&acc)[VPL][VW]) {
         float* c = carry + a * (long long)F;

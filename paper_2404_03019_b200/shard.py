@@ -1,5 +1,6 @@
 """Multi-GPU host logic (H9): segment-boundary shards, the
-max-over-ranks step time, and the optional output all-gather.
+max-over-ranks step time, the optional output all-gather (NCCL), and the
+peer-replica mapping of the fused all-gather epilogue (f4).
 
 The reduction itself needs no collective: rank p owns output rows
 [s_p, s_{p+1}) and edges [e_p, e_{p+1}) of the partition computed by
@@ -60,3 +61,25 @@ def allgather_rows(local_out, seg_bounds: Sequence[int], group=None):
     parts = [torch.empty_like(pad) for _ in range(P)]
     dist.all_gather(parts, pad, group=group)
     return torch.cat([parts[p][: counts[p]] for p in range(P)], dim=0)
+
+
+def open_peer_replicas(local_full, group=None):
+    """f4 plumbing: map every rank's full-output replica into this process.
+
+    Each rank allocates its replica ([total_segments, F], contiguous) and calls
+    this collectively; the CUDA IPC handles travel with all_gather_object and
+    are opened here (peer access over NVLink is enabled lazily by the IPC
+    open).  Returns the replicas in rank order (this rank's own tensor at its
+    index) — the `outs` of geot_segment_reduce_allgather, which then writes
+    this rank's rows into all of them.  Keep the returned tensors alive while
+    peers may write; order reads after a stream sync + barrier on every rank."""
+    import torch.distributed as dist
+    from torch.multiprocessing.reductions import reduce_tensor
+    if not local_full.is_cuda or not local_full.is_contiguous():
+        raise ValueError("the replica must be a contiguous CUDA tensor")
+    handle = reduce_tensor(local_full)
+    objs = [None] * dist.get_world_size(group)
+    dist.all_gather_object(objs, handle, group=group)
+    me = dist.get_rank(group)
+    return [local_full if r == me else fn(*args) for r, (fn, args) in enumerate(objs)]
+
