@@ -117,10 +117,11 @@ cudaError_t run_edge_tile(const EdgeTileParams& p, int ctas_per_sm, int nsm, cud
 // agent owns >= 1 row).  Agent count = carry slots.
 long long stream_agents(long long nnz, int lpr, int warps, int nsm, int ctas_per_sm);
 
-template <typename T, int VW, int LPR, int VPL, bool ISMAX, int W, int RS, int NS, int MODE = 0, bool SRC64 = false>
+template <typename T, int VW, int LPR, int VPL, bool ISMAX, int W, int RS, int NS, int MODE = 0, bool SRC64 = false,
+          bool REP = false>
 cudaError_t run_stream(const StreamParams& p, const EdgeTileParams& fix, int nsm, cudaStream_t st) {
     constexpr int G = 32 / LPR;
-    auto kern = stream_kernel<T, VW, LPR, VPL, ISMAX, W, RS, NS, MODE, SRC64>;
+    auto kern = stream_kernel<T, VW, LPR, VPL, ISMAX, W, RS, NS, MODE, SRC64, REP>;
     const size_t smem = stream_smem_bytes(W, NS, G, RS, p.row_bytes, MODE);
     if (smem > 227 * 1024) return cudaErrorNotSupported;
     const int occ = cached_occupancy(kern, W * 32, smem);
@@ -147,6 +148,22 @@ cudaError_t launch_stream(const StreamParams& p, const EdgeTileParams& fix, int 
                           int ns, bool ismax, int nsm, cudaStream_t st) {
     constexpr int WIDE = 16 / (int)sizeof(T);
     if (vw != WIDE) return cudaErrorNotSupported;
+    if (p.outs.n > 1) {  // f4 replicas: the default pipeline of each lane shape
+#define GEOT_RSHAPE(LPR_, VPL_, W_, RS_, NS_)                                                              \
+    if (lpr == LPR_ && vpl == VPL_)                                                                        \
+        return ismax ? run_stream<T, WIDE, LPR_, VPL_, true, W_, RS_, NS_, 0, false, true>(p, fix, nsm, st)  \
+                     : run_stream<T, WIDE, LPR_, VPL_, false, W_, RS_, NS_, 0, false, true>(p, fix, nsm, st);
+        GEOT_RSHAPE(8, 1, 16, 6, 4)
+        GEOT_RSHAPE(16, 1, 16, 6, 4)
+        GEOT_RSHAPE(32, 1, 16, 6, 4)
+        GEOT_RSHAPE(32, 2, 16, 3, 4)
+        GEOT_RSHAPE(32, 4, 8, 3, 4)
+        if constexpr (sizeof(T) == 4) {
+            GEOT_RSHAPE(32, 8, 8, 1, 4)
+        }
+#undef GEOT_RSHAPE
+        return cudaErrorNotSupported;
+    }
 #define GEOT_SSHAPE(LPR_, VPL_, W_, RS_, NS_)                                                        \
     if (lpr == LPR_ && vpl == VPL_ && w == W_ && rs == RS_ && ns == NS_)                             \
         return ismax ? run_stream<T, WIDE, LPR_, VPL_, true, W_, RS_, NS_>(p, fix, nsm, st)          \

@@ -99,7 +99,8 @@ __device__ __forceinline__ void cp_async_16_zfill(uint32_t dst, const void* src,
 // buffer is refilled.  MODE 2 also stages w[e] and folds w[e] * x[src[e]].  An
 // out-of-range src id gathers a zero row (memory-safe; results for bad data
 // are unspecified).
-template <typename T, int VW, int LPR, int VPL, bool ISMAX, int W, int RS, int NS, int MODE = 0, bool SRC64 = false>
+template <typename T, int VW, int LPR, int VPL, bool ISMAX, int W, int RS, int NS, int MODE = 0, bool SRC64 = false,
+          bool REP = false>
 __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const StreamParams p) {
     constexpr bool TMA = NS > 0;
     static_assert(MODE == 0 || NS > 0, "the fused forms use the shared-memory ring");
@@ -301,11 +302,12 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
             for (int j = 0; j < VPL; ++j)
                 if (vec_col(j) < p.NV) st_vec(reinterpret_cast<Raw*>(rowp + vec_col(j) * VW), packed[j]);
         }
-        for (int d = 1; d < p.outs.n; ++d) {  // replicas (f4)
-            T* rowp = static_cast<T*>(p.outs.ptr[d]) + (key - p.outs.row_off) * (long long)F;
-#pragma unroll
-            for (int j = 0; j < VPL; ++j)
-                if (vec_col(j) < p.NV) st_vec(reinterpret_cast<Raw*>(rowp + vec_col(j) * VW), packed[j]);
+        if constexpr (REP) {  // f4: the same row into every replica
+            for (int d = 1; d < p.outs.n; ++d) {
+                T* rp = static_cast<T*>(p.outs.ptr[d]) + (key - p.outs.row_off) * (long long)F;
+                for (int j = 0; j < VPL; ++j)
+                    if (vec_col(j) < p.NV) st_vec(reinterpret_cast<Raw*>(rp + vec_col(j) * VW), packed[j]);
+            }
         }
     };
     auto gap_fill = [&](long long lo_k, long long hi_k) {
@@ -315,16 +317,23 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
 #pragma unroll
         for (int q = 0; q < VW; ++q) z[q] = 0.0f;
         const Raw zr = Cv::pack(z);
-        for (int d = 0; d < p.outs.n; ++d)
-            for (long long r = r0; r < r1; ++r) {
-                T* rowp = (d == 0 ? out + (r - seg_lo) * (long long)F
-                                  : static_cast<T*>(p.outs.ptr[d]) + (r - p.outs.row_off) * (long long)F);
+        for (long long r = r0; r < r1; ++r) {
+            T* rowp = out + (r - seg_lo) * (long long)F;
 #pragma unroll
-                for (int j = 0; j < VPL; ++j) {
-                    const int v = vec_col(j);
-                    if (v < p.NV) st_vec(reinterpret_cast<Raw*>(rowp + v * VW), zr);
+            for (int j = 0; j < VPL; ++j) {
+                const int v = vec_col(j);
+                if (v < p.NV) st_vec(reinterpret_cast<Raw*>(rowp + v * VW), zr);
+            }
+        }
+        if constexpr (REP) {
+            for (int d = 1; d < p.outs.n; ++d) {
+                for (long long r = r0; r < r1; ++r) {
+                    T* rp = static_cast<T*>(p.outs.ptr[d]) + (r - p.outs.row_off) * (long long)F;
+                    for (int j = 0; j < VPL; ++j)
+                        if (vec_col(j) < p.NV) st_vec(reinterpret_cast<Raw*>(rp + vec_col(j) * VW), zr);
                 }
             }
+        }
     };
     auto carry_store = [&](float* carry, const float (&acc)[VPL][VW]) {
         float* c = carry + a * (long long)F;
