@@ -1,5 +1,2 @@
-for i in 1 2; do
-(cd abold && python bench.py --no-cpu-baseline 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('OLD', d['value'], d['roofline']['kernel_ms'])")
-python bench.py --no-cpu-baseline 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('NEW', d['value'], d['roofline']['kernel_ms'])"
-done
-timeout 900 python -m pytest tests/test_gpu_allgather.py tests/test_gpu_parity.py -m gpu -q -x 2>&1 | tail -2
+(cd abold && python ../tools/quick_perf.py 2>&1 | tail -17 | cut -c1-120 | sed 's/^/OLD /')
+python tools/quick_perf.py 2>&1 | tail -17 | cut -c1-120 | sed 's/^/NEW /'
