@@ -105,7 +105,8 @@ __global__ void zero_fill_kernel(unsigned char* out, long long bytes) {
 // every call and variant, so stale bytes of other regions can never be read as
 // a flag; they must be zero before the workspace's first use.
 static int sm_count();
-static size_t ws_flag_bytes() { return align_up((size_t)sm_count() * 16 * 4 * sizeof(unsigned long long), 256); }
+// one flag per agent: up to 16 warps x 8 agents per CTA, 2 CTAs per SM
+static size_t ws_flag_bytes() { return align_up((size_t)sm_count() * 16 * 8 * 2 * sizeof(unsigned long long), 256); }
 struct WsLayout {
     size_t ctrl = 0, flags = 0, meta = 0, carry_h = 0, carry_t = 0, total = 0;
 };

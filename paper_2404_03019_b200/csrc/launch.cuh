@@ -153,6 +153,7 @@ cudaError_t launch_stream(const StreamParams& p, const EdgeTileParams& fix, int 
     if (lpr == LPR_ && vpl == VPL_)                                                                        \
         return ismax ? run_stream<T, WIDE, LPR_, VPL_, true, W_, RS_, NS_, 0, false, true>(p, fix, nsm, st)  \
                      : run_stream<T, WIDE, LPR_, VPL_, false, W_, RS_, NS_, 0, false, true>(p, fix, nsm, st);
+        GEOT_RSHAPE(4, 1, 16, 4, 4)
         GEOT_RSHAPE(8, 1, 16, 6, 4)
         GEOT_RSHAPE(16, 1, 16, 6, 4)
         GEOT_RSHAPE(32, 1, 16, 6, 4)
@@ -175,6 +176,9 @@ cudaError_t launch_stream(const StreamParams& p, const EdgeTileParams& fix, int 
     GEOT_SSHAPE(LPR_, 1, 8, 8, 6)    \
     GEOT_SSHAPE(LPR_, 1, 8, 4, 0)    \
     GEOT_SSHAPE(LPR_, 1, 8, 8, 0)
+    GEOT_SSHAPE(4, 1, 16, 4, 4) /* 64-byte rows: 8 agents per warp */
+    GEOT_SSHAPE(4, 1, 8, 4, 8)
+    GEOT_SSHAPE(4, 1, 8, 4, 0)
     GEOT_SSHAPE_V1(8)
     GEOT_SSHAPE_V1(16)
     GEOT_SSHAPE_V1(32)
@@ -211,6 +215,7 @@ cudaError_t launch_stream_gather(const StreamParams& p, const EdgeTileParams& fi
             GEOT_GSHAPE_I(LPR_, W_, RS_, NS_, false)                                                           \
         }                                                                                                      \
     }
+    GEOT_GSHAPE(4, 16, 4, 4)
     GEOT_GSHAPE(8, 16, 6, 4)
     GEOT_GSHAPE(16, 16, 6, 4)
     GEOT_GSHAPE(32, 16, 6, 4)

@@ -310,6 +310,30 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
             }
         }
     };
+    // predicated form of write_row (no branch around the store)
+    auto write_row_pred = [&](bool pred, long long key, const float (&acc)[VPL][VW], long long count) {
+        const bool ok = pred && key >= seg_lo && key < seg_hi;
+        Raw packed[VPL];
+#pragma unroll
+        for (int j = 0; j < VPL; ++j) {
+            float o[VW];
+#pragma unroll
+            for (int q = 0; q < VW; ++q) o[q] = finalize(acc[j][q], p.op, count);
+            packed[j] = Cv::pack(o);
+        }
+        T* rowp = out + (key - seg_lo) * (long long)F;
+#pragma unroll
+        for (int j = 0; j < VPL; ++j)
+            if (ok && vec_col(j) < p.NV) st_vec(reinterpret_cast<Raw*>(rowp + vec_col(j) * VW), packed[j]);
+        if constexpr (REP) {
+            if (ok)
+                for (int d = 1; d < p.outs.n; ++d) {
+                    T* rp = static_cast<T*>(p.outs.ptr[d]) + (key - p.outs.row_off) * (long long)F;
+                    for (int j = 0; j < VPL; ++j)
+                        if (vec_col(j) < p.NV) st_vec(reinterpret_cast<Raw*>(rp + vec_col(j) * VW), packed[j]);
+                }
+        }
+    };
     auto gap_fill = [&](long long lo_k, long long hi_k) {
         long long r0 = (lo_k < seg_lo) ? seg_lo : lo_k + 1;
         long long r1 = (hi_k > seg_hi) ? seg_hi : hi_k;
@@ -370,9 +394,44 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
                        long long r_base, float wmine) {
 #pragma unroll
         for (int r = 0; r < SUB; ++r) {
-            if (r >= cnt) break;
+            // (G >= 4: no early exit — the warp-wide votes below need every lane)
+            if constexpr (G < 4) {
+                if (r >= cnt) break;
+            }
+            const bool valid = r < cnt;
             const Raw (&raw)[VPL] = rows[r];
-            if ((heads >> r) & 1u) {  // segment `cur` ended at the previous row
+            if constexpr (G >= 4) {
+                // small rows, 4+ agents per warp: their segment ends rarely coincide, so
+                // a branch per end would serialise the warp — the end of a segment is
+                // handled branch-free (predicated store, selects); only the rare
+                // events (head-partial capture, gaps) take warp-uniform branches
+                const bool h = valid && ((heads >> r) & 1u);
+                const long long k = __shfl_sync(0xffffffffu, kmine, (koff + r) & (LPR - 1), LPR);
+                const long long e = r_base + r;
+                const bool hf = h && first && head_open;
+                if (__any_sync(0xffffffffu, hf)) {
+                    if (hf) {
+#pragma unroll
+                        for (int j = 0; j < VPL; ++j)
+#pragma unroll
+                            for (int q = 0; q < VW; ++q) hacc[j][q] = acc[j][q];
+                        flags |= TM_HEAD_OPEN;
+                        head_end = e;
+                    }
+                }
+                write_row_pred(h && !hf, cur, acc, e - seg_start);
+                const bool gp = h && k != cur + 1;
+                if (__any_sync(0xffffffffu, gp)) {
+                    if (gp) gap_fill(cur, k);
+                }
+                first = first && !h;
+                cur = h ? k : cur;
+                seg_start = h ? e : seg_start;
+#pragma unroll
+                for (int j = 0; j < VPL; ++j)
+#pragma unroll
+                    for (int q = 0; q < VW; ++q) acc[j][q] = h ? identity<ISMAX>() : acc[j][q];
+            } else if ((heads >> r) & 1u) {  // segment `cur` ended at the previous row
                 const long long k = __shfl_sync(gmask, kmine, koff + r, LPR);
                 const long long e = r_base + r;
                 if (first && head_open) {
@@ -393,6 +452,9 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
                 for (int j = 0; j < VPL; ++j)
 #pragma unroll
                     for (int q = 0; q < VW; ++q) acc[j][q] = identity<ISMAX>();
+            }
+            if constexpr (G >= 4) {
+                if (!valid) continue;  // (no collective below this point)
             }
             float wr = 1.0f;
             if constexpr (MODE == 2) wr = __shfl_sync(gmask, wmine, koff + r, LPR);
@@ -494,19 +556,19 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
                                     : Raw{};
             nkey = (li < c) ? load_index(p.idx, p.idx64, rb + li) : KEY_AFTER;
         };
-        if (nst > 0) fetch(0);
+        if (nst_w > 0) fetch(0);
 #pragma unroll 1
-        for (int s = 0; s < nst; ++s) {
+        for (int s = 0; s < nst_w; ++s) {  // warp-uniform trip count (groups past their range idle)
             Raw rows[RS][VPL];
 #pragma unroll
             for (int r = 0; r < RS; ++r)
 #pragma unroll
                 for (int j = 0; j < VPL; ++j) rows[r][j] = nxt[r][j];
             const long long kmine = nkey;
-            if (s + 1 < nst) fetch(s + 1);
+            if (s + 1 < nst_w) fetch(s + 1);
             const long long r_base = e_lo + (long long)s * RS;
             int cnt = (int)(e_hi - r_base);
-            cnt = cnt > RS ? RS : cnt;
+            cnt = cnt < 0 ? 0 : (cnt > RS ? RS : cnt);
             long long kprev = __shfl_up_sync(gmask, kmine, 1, LPR);
             if (li == 0) kprev = cur;
             const unsigned heads = __ballot_sync(gmask, li < cnt && kmine != kprev) >> (gi * LPR);

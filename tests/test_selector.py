@@ -63,6 +63,7 @@ def test_codegen_matches_tree(L):
 STREAM_PIPES = {1: {(16, 6, 4), (8, 6, 8), (16, 3, 8), (8, 8, 6), (8, 4, 1), (8, 8, 1)},
                 2: {(16, 3, 4), (8, 3, 8), (8, 4, 1)}, 4: {(8, 3, 4), (8, 2, 1)},
                 8: {(8, 1, 4), (8, 1, 6), (8, 1, 1)}}
+STREAM_PIPES_LPR4 = {(16, 4, 4), (8, 4, 8), (8, 4, 1)}  # 64-byte rows: RS <= 4
 
 
 def test_select_config_always_valid(L):
@@ -77,11 +78,13 @@ def test_select_config_always_valid(L):
                         assert L.geot_select_config(nnz, S, F, 0, dt, 0, fused, ctypes.byref(c)) == 0
                         wide = 4 if dt == 0 else 8
                         if c.variant == 3:  # 16-byte lane vectors, 8/16/32 lanes per row
-                            assert c.vec_elems == wide and c.lanes_per_row >= 8
+                            assert c.vec_elems == wide and c.lanes_per_row >= 4
+                            rs_def = min(6, c.lanes_per_row)
                             assert not fused or (c.vecs_per_lane == 1 and (c.warps_per_cta, c.rows_per_group, c.stages)
-                                                 == (16, 6, 4))
+                                                 == (16, rs_def, 4))
                             assert F // wide <= c.lanes_per_row * c.vecs_per_lane
-                            assert (c.warps_per_cta, c.rows_per_group, c.stages) in STREAM_PIPES[c.vecs_per_lane]
+                            pipes = STREAM_PIPES_LPR4 if c.lanes_per_row == 4 else STREAM_PIPES[c.vecs_per_lane]
+                            assert (c.warps_per_cta, c.rows_per_group, c.stages) in pipes
                         elif c.variant == 2:
                             assert not fused and (F in (1, 2, 4, 8) or (dt == 1 and F == 16))
                         else:

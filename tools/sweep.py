@@ -77,10 +77,10 @@ STREAM_PIPES = {1: [(16, 6, 4), (8, 6, 8), (16, 3, 8), (8, 8, 6), (8, 4, 1), (8,
 def stream_lane_shape(F, dtype):
     """(lanes per row, vectors per lane) of the stream kernel for F, or None (select.cpp)."""
     wide = 4 if dtype == "f32" else 8
-    if F % wide or F // wide < 8:
+    if F % wide or F // wide < 4:
         return None
     nv = F // wide
-    lpr = 8
+    lpr = 4
     while lpr < nv and lpr < 32:
         lpr *= 2
     v = 1
@@ -105,7 +105,8 @@ def candidate_configs(E, S, F, dtype, fused, quick=False):
     if narrow_ok:
         out.append({"variant": 2})
     if stream_ok:
-        for (w, rs, ns) in STREAM_PIPES[shape[1]]:
+        pipes = [(16, 4, 4), (8, 4, 8), (8, 4, 1)] if shape[0] == 4 else STREAM_PIPES[shape[1]]
+        for (w, rs, ns) in pipes:
             if rs <= shape[0]:
                 out.append({"variant": 3, "warps_per_cta": w, "rows_per_group": rs, "stages": ns})
     return base, out
