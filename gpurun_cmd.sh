@@ -1,9 +1,3 @@
-T="timeout 60"
-for F in 32; do for d in powerlaw uniform; do
-(cd abold && $T python ../tools/time_cfgs.py 16777216 1048576 $F f32 $d -- '' | sed 's/^/OLD /')
-$T python tools/time_cfgs.py 16777216 1048576 $F f32 $d -- '' | sed 's/^/NEW /'
-done; done
-(cd abold && $T python ../tools/time_cfgs.py 16777216 1048576 64 bf16 powerlaw -- '' | sed 's/^/OLD /')
-$T python tools/time_cfgs.py 16777216 1048576 64 bf16 powerlaw -- '' | sed 's/^/NEW /'
-(cd abold && $T python ../tools/time_cfgs.py 16777216 1048576 16 f32 uniform -- '' | sed 's/^/OLD /')
-$T python tools/time_cfgs.py 16777216 1048576 16 f32 uniform -- '' '{"variant":3}' | sed 's/^/NEW /'
+timeout 2700 python tools/sweep.py --grid selector --out gpurun_out/perfdb_r1b.jsonl > gpurun_out/sweep_r1b.log 2>&1; echo "sweep rc=$?"
+timeout 900 python tools/sweep.py --grid selector_large --out gpurun_out/perfdb_r1b.jsonl >> gpurun_out/sweep_r1b.log 2>&1; echo "sweep-large rc=$?"
+wc -l gpurun_out/perfdb_r1b.jsonl

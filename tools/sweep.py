@@ -101,11 +101,13 @@ def candidate_configs(E, S, F, dtype, fused, quick=False):
     esz = 4 if dtype == "f32" else 2
     narrow_ok = (not fused) and E >= 65536 and (F in (1, 2, 4, 8) or (dtype == "bf16" and F == 16))
     shape = stream_lane_shape(F, dtype)
-    stream_ok = (not fused) and E >= 65536 and shape is not None
+    stream_ok = E >= 65536 and shape is not None and (not fused or shape[1] == 1)
     if narrow_ok:
         out.append({"variant": 2})
     if stream_ok:
         pipes = [(16, 4, 4), (8, 4, 8), (8, 4, 1)] if shape[0] == 4 else STREAM_PIPES[shape[1]]
+        if fused:  # the gather form: one pipeline per lane shape (launch.cuh)
+            pipes = [(16, min(6, shape[0]), 4)]
         for (w, rs, ns) in pipes:
             if rs <= shape[0]:
                 out.append({"variant": 3, "warps_per_cta": w, "rows_per_group": rs, "stages": ns})
@@ -163,13 +165,13 @@ def selector_grid():
                 continue
             for avg in (3, 16, 64):
                 g.append((E, max(1, E // avg), F, "f32", "powerlaw", "sum", False))
-    for F in (8, 64, 128, 256):
+    for F in (8, 16, 32, 64, 128, 256):
         for logE in (20, 23):
             g.append((1 << logE, (1 << logE) // 16, F, "bf16", "powerlaw", "sum", False))
     for F in (4, 64, 128):
         g.append((1 << 22, (1 << 22) // 16, F, "f32", "uniform", "sum", False))
-    for F in (16, 64, 128):
-        for avg in (8, 64):
+    for F in (16, 32, 64, 128):
+        for avg in (8, 64, 492):
             g.append((1 << 23, (1 << 23) // avg, F, "f32", "powerlaw", "sum", True))
     # small graphs (Cora/Citeseer/PubMed-sized) and arxiv-sized ones
     for F in (8, 16, 32, 64, 128):
