@@ -133,8 +133,9 @@ def test_forced_configs(geot, R, vw, F):
 STREAM = 3  # GEOT_VARIANT_STREAM
 
 
-@pytest.mark.parametrize("F,dtype", [(32, "f32"), (64, "f32"), (96, "f32"), (128, "f32"), (256, "f32"),
-                                     (1024, "f32"), (64, "bf16"), (128, "bf16"), (512, "bf16")])
+@pytest.mark.parametrize("F,dtype", [(16, "f32"), (32, "f32"), (64, "f32"), (96, "f32"), (128, "f32"),
+                                     (256, "f32"), (1024, "f32"), (32, "bf16"), (64, "bf16"), (128, "bf16"),
+                                     (512, "bf16")])
 @pytest.mark.parametrize("op", ["sum", "mean", "max"])
 def test_stream_variant(geot, F, dtype, op):
     E = 70_000 if F <= 256 else 66_000
@@ -142,8 +143,25 @@ def test_stream_variant(geot, F, dtype, op):
         parity(geot, E, E // 7, F, op, dtype, mode, "powerlaw15", seed=F, cfg={"variant": STREAM})
 
 
+# every compiled pipeline (W warps, RS rows per stage, NS stages; NS=1 is the
+# LDG register pipeline) of every lane shape (LPR 4/8/16/32, VPL 1..8)
+PIPES = {4: [(16, 4, 4), (8, 4, 8), (8, 4, 1)],
+         1: [(16, 6, 4), (8, 6, 8), (16, 3, 8), (8, 8, 6), (8, 4, 1), (8, 8, 1)],
+         2: [(16, 3, 4), (8, 3, 8), (8, 4, 1)], 4.5: [(8, 3, 4), (8, 2, 1)], 8: [(8, 1, 4), (8, 1, 6), (8, 1, 1)]}
+
+
+@pytest.mark.parametrize("F,key", [(16, 4), (32, 1), (64, 1), (128, 1), (256, 2), (512, 4.5), (1024, 8)])
+def test_stream_every_pipeline(geot, F, key):
+    for (w, rs, ns) in PIPES[key]:
+        if rs > max(4, min(32, F // 4)):
+            continue
+        cfg = {"variant": STREAM, "warps_per_cta": w, "rows_per_group": rs, "stages": ns}
+        for op in ("sum", "max"):
+            parity(geot, 90_001, 9_000, F, op, "f32", "int", "powerlaw15", seed=F + w + rs + ns, cfg=cfg)
+
+
 @pytest.mark.parametrize("kind", synth.STRESS_KINDS)
-@pytest.mark.parametrize("F", [32, 128, 512])
+@pytest.mark.parametrize("F", [16, 32, 128, 512])
 def test_stream_stress(geot, kind, F):
     cfg = {"variant": STREAM}
     for op in ("sum", "mean", "max"):
@@ -283,19 +301,17 @@ def fused_case(E, S, V, F, dtype, mode, kind, seed):
     return L, dst, src, x
 
 
-@pytest.mark.parametrize("F,dtype", [(32, "f32"), (64, "f32"), (128, "f32"), (64, "bf16"), (128, "bf16"),
-                                     (256, "bf16")])
+@pytest.mark.parametrize("F,dtype", [(16, "f32"), (32, "f32"), (64, "f32"), (128, "f32"), (32, "bf16"),
+                                     (64, "bf16"), (128, "bf16"), (256, "bf16")])
 @pytest.mark.parametrize("op", ["sum", "mean", "max"])
 def test_fused_gather_stream(geot, F, dtype, op):
     V, E, S = 20_000, 200_003, 15_000
-    tdt = torch.float32 if dtype == "f32" else torch.bfloat16
-    assert geot.geot_select_config(E, S, F, op, tdt, torch.int32, True).variant == 3
     for mode in (("signed",) if op == "max" else ("int", "real")):
         L, dst, src, x = fused_case(E, S, V, F, dtype, mode, "powerlaw15", F + 3)
         ref = oracle.gather_segment_reduce(x, src, dst, S, op, nthreads=oracle.default_threads())
         for it in (torch.int32, torch.int64):
-            y = geot.index_segment_reduce(torch.from_numpy(src).to(it).cuda(), torch.from_numpy(dst).to(it).cuda(),
-                                          to_torch_vals(x), op, num_segments=S)
+            y = geot.geot_gather_segment_reduce(to_torch_vals(x), torch.from_numpy(src).to(it).cuda(),
+                                                torch.from_numpy(dst).to(it).cuda(), S, op, cfg={"variant": 3})
             check(from_torch_vals(y), ref, op, dtype, mode, counts=L, what=f"gather-stream F={F} {dtype} {op} {it}")
 
 

@@ -122,7 +122,9 @@ def run(args):
     grid = GRIDS[args.grid]
     for (E, S, F, dtype, dist, op, fused) in grid:
         seed = 7
-        V = S
+        # fused: x has >= 2^18 rows (a Reddit-sized feature matrix) so a high mean
+        # degree does not make x trivially cache-resident (V is not a selector feature)
+        V = max(S, 1 << 18) if fused else S
         L, idx, X, src = make_inputs(E, S, F, dtype, dist, seed, fused, V)
         esz = 4 if dtype == "f32" else 2
         B = E * F * esz + E * 4 * (2 if fused else 1) + S * F * esz
@@ -196,8 +198,13 @@ def selector_grid_large():
     return g
 
 
+def selector_grid_fused():
+    return [w for w in selector_grid() if w[6]]
+
+
 GRIDS = {
     "selector": selector_grid(),
+    "selector_fused": selector_grid_fused(),
     "selector_large": selector_grid_large(),
     "arxiv": [(ARXIV[0], ARXIV[1], 128, "f32", "powerlaw", "sum", False)],
     "main": [
