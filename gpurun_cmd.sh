@@ -1,2 +1,2 @@
-timeout 900 python tools/sweep.py --grid selector_fused --out gpurun_out/perfdb_r1c.jsonl > gpurun_out/sweep_r1c.log 2>&1; echo "sweep rc=$?"
-wc -l gpurun_out/perfdb_r1c.jsonl
+bash tools/gpu_round.sh r1e
+timeout 900 python tools/report_configs.py --md gpurun_out/r1e_configs.md --jsonl gpurun_out/r1e_configs.jsonl > gpurun_out/r1e_configs.log 2>&1; echo "configs rc=$?"
