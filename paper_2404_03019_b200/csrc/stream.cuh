@@ -497,8 +497,14 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
             const long long r_base = e_lo + (long long)s * RS;
             int cnt = (int)(e_hi - r_base);
             cnt = cnt < 0 ? 0 : (cnt > RS ? RS : cnt);
-            const long long kmine = (li < cnt) ? gkey[li] : KEY_AFTER;
-            const long long kprev = (li == 0) ? cur : ((li <= cnt) ? gkey[li - 1] : KEY_AFTER);
+            // int32 keys sit in the low half of 8-byte slots: sign-extend them, so
+            // they compare equal to the load_index() copies (prevk / nextk) — a
+            // zero-extended negative key would break the carry chain's consistency
+            auto slot_key = [&](int i) -> long long {
+                return isz == 4 ? (long long)(int)(unsigned)gkey[i] : gkey[i];
+            };
+            const long long kmine = (li < cnt) ? slot_key(li) : KEY_AFTER;
+            const long long kprev = (li == 0) ? cur : ((li <= cnt) ? slot_key(li - 1) : KEY_AFTER);
             float wmine = 1.0f;
             if constexpr (MODE == 2) wmine = (li < cnt) ? wring[(b * G + gi) * RS + li] : 0.0f;
             // is_seg of the whole stage (Alg. 1): row r starts a segment iff its

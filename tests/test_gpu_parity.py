@@ -248,6 +248,41 @@ def test_misaligned_pointers_use_scalar_path(geot):
     check(y.cpu().numpy(), ref, "sum", "f32", "int")
 
 
+@pytest.mark.parametrize("variant,F,dtype", [(2, 1, "f32"), (2, 4, "f32"), (2, 16, "bf16"), (3, 16, "f32"),
+                                             (3, 64, "f32"), (3, 128, "bf16"), (1, 3, "f32"), (1, 64, "f32")])
+def test_bad_data_stays_in_bounds(geot, variant, F, dtype):
+    """Unsorted keys, keys outside [0, S) and (fused) src ids outside [0, V): results
+    are unspecified (P:328 precondition) but every kernel must stay memory-safe —
+    no fault, and no store outside `out` (guard rows around it keep their bits)."""
+    rng = np.random.default_rng(F + variant)
+    # (unsorted keys make every head a "gap" of up to S rows: keep S small, the
+    # zero-fill work of garbage input is O(E * S))
+    E, S, V, pad = 100_000, 400, 5_000, 64
+    tdt = torch.float32 if dtype == "f32" else torch.bfloat16
+    idx = torch.from_numpy(rng.integers(-30, S + 30, E).astype(np.int32)).cuda()
+    idx_sorted_bad = torch.sort(idx).values  # sorted, but with out-of-range keys at both ends
+    for keys in (idx, idx_sorted_bad):
+        big = torch.full((S + 2 * pad, F), 7.0, dtype=tdt, device="cuda")
+        X = torch.ones((E, F), dtype=tdt, device="cuda")
+        for op in ("sum", "mean", "max"):
+            try:
+                geot.geot_segment_reduce(X, keys, S, op, out=big[pad:pad + S], cfg={"variant": variant})
+            except geot.GeotError as ex:  # a variant may not apply to the shape: that is fine
+                assert ex.status == 2, ex
+            torch.cuda.synchronize()
+            assert torch.all(big[:pad] == 7.0) and torch.all(big[pad + S:] == 7.0), (variant, F, op)
+        if variant != 2:  # fused form (no narrow variant)
+            x = torch.ones((V, F), dtype=tdt, device="cuda")
+            src = torch.from_numpy(rng.integers(-300, V + 300, E).astype(np.int32)).cuda()
+            big.fill_(7.0)
+            try:
+                geot.geot_gather_segment_reduce(x, src, keys, S, "sum", out=big[pad:pad + S], cfg={"variant": variant})
+            except geot.GeotError as ex:
+                assert ex.status == 2, ex
+            torch.cuda.synchronize()
+            assert torch.all(big[:pad] == 7.0) and torch.all(big[pad + S:] == 7.0), (variant, F, "fused")
+
+
 def test_determinism(geot):
     L, idx, X = make_case(200_000, 5_000, 64, "f32", "real", "powerlaw15", 11)
     xt, it = to_torch_vals(X), torch.from_numpy(idx).to(torch.int32).cuda()
