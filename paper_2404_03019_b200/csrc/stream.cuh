@@ -374,6 +374,26 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
     for (int j = 0; j < VPL; ++j)
 #pragma unroll
         for (int q = 0; q < VW; ++q) acc[j][q] = identity<ISMAX>();
+    // bf16 max (branchy path): fold packed bf16 pairs with HMNMX2 (exact: the max is
+    // one of the inputs) and widen to the fp32 acc only where a segment ends
+    constexpr bool PKMAX = ISMAX && sizeof(T) == 2 && MODE == 0 && G < 4;
+    constexpr int PKW = PKMAX ? VW / 2 : 1;
+    uint32_t pk[VPL][PKW];
+#pragma unroll
+    for (int j = 0; j < VPL; ++j)
+#pragma unroll
+        for (int w = 0; w < PKW; ++w) pk[j][w] = 0xFF80FF80u;  // bf16 -inf, -inf
+    auto sync_acc = [&]() {
+        if constexpr (PKMAX) {
+#pragma unroll
+            for (int j = 0; j < VPL; ++j)
+#pragma unroll
+                for (int w = 0; w < PKW; ++w) {
+                    acc[j][2 * w] = __uint_as_float(pk[j][w] << 16);
+                    acc[j][2 * w + 1] = __uint_as_float(pk[j][w] & 0xFFFF0000u);
+                }
+        }
+    };
 
     long long cur = first_key;
     const bool head_open = nrows > 0 && prevk == cur;
@@ -434,6 +454,7 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
             } else if ((heads >> r) & 1u) {  // segment `cur` ended at the previous row
                 const long long k = __shfl_sync(gmask, kmine, koff + r, LPR);
                 const long long e = r_base + r;
+                sync_acc();
                 if (first && head_open) {
 #pragma unroll
                     for (int j = 0; j < VPL; ++j)
@@ -452,12 +473,32 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
                 for (int j = 0; j < VPL; ++j)
 #pragma unroll
                     for (int q = 0; q < VW; ++q) acc[j][q] = identity<ISMAX>();
+                if constexpr (PKMAX) {
+#pragma unroll
+                    for (int j = 0; j < VPL; ++j)
+#pragma unroll
+                        for (int w = 0; w < PKW; ++w) pk[j][w] = 0xFF80FF80u;
+                }
             }
             if constexpr (G >= 4) {
                 if (!valid) continue;  // (no collective below this point)
             }
             float wr = 1.0f;
             if constexpr (MODE == 2) wr = __shfl_sync(gmask, wmine, koff + r, LPR);
+            if constexpr (PKMAX) {
+#pragma unroll
+                for (int j = 0; j < VPL; ++j) {
+                    const uint32_t* rw = reinterpret_cast<const uint32_t*>(&raw[j]);
+#pragma unroll
+                    for (int w = 0; w < PKW; ++w) {
+                        __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(&pk[j][w]);
+                        const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(&rw[w]);
+                        a = __hmax2(a, b);
+                        pk[j][w] = *reinterpret_cast<const uint32_t*>(&a);
+                    }
+                }
+                continue;
+            }
 #pragma unroll
             for (int j = 0; j < VPL; ++j) {
                 float f[VW];
@@ -583,6 +624,7 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
     }
 
     // ---- agent end: publish the carries later agents need (H5) ...
+    sync_acc();
     if (nrows > 0) {
         const bool tail_open = (nextk == cur);
         if (first && head_open) {
