@@ -1,4 +1,5 @@
-bash tools/gpu_round.sh r1f
-timeout 900 python tools/report_configs.py --md gpurun_out/r1f_configs.md --jsonl gpurun_out/r1f_configs.jsonl > gpurun_out/r1f_configs.log 2>&1; echo "configs rc=$?"
-bash tools/gpu_prof4.sh r1f "narrow f1 16777216 1048576 1 f32 powerlaw" "stream_kernel reddit 114615892 232965 64 f32 powerlaw - fused" "stream_kernel products 61859140 2449029 128 bf16 powerlaw"
-ls -la gpurun_out | head -30
+timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "bad_data or stream or int64" 2>&1 | tail -2
+for i in 1 2; do
+(cd abold && python bench.py --no-cpu-baseline 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('OLD', d['value'], d['roofline']['kernel_ms'])")
+python bench.py --no-cpu-baseline 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('NEW', d['value'], d['roofline']['kernel_ms'])"
+done

@@ -281,9 +281,19 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
         for (int s = 0; s < NS && s < nst_w; ++s) issue(s, 0);
     }
 
-    const long long prevk = (e_lo > 0) ? load_index(p.idx, p.idx64, e_lo - 1) : KEY_BEFORE;
-    const long long nextk = (e_hi < p.E) ? load_index(p.idx, p.idx64, e_hi) : KEY_AFTER;
-    const long long first_key = (nrows > 0) ? load_index(p.idx, p.idx64, e_lo) : KEY_AFTER;
+    // Every key is read the way the key ring holds it: int32 keys ZERO-extended
+    // (they land in the low half of zeroed 8-byte slots).  Keys must compare the
+    // same wherever they were read — the carry chain's head/tail tests pair a
+    // ring copy with these direct loads (a sign/zero mismatch on a negative key
+    // once deadlocked it).  Negative int32 keys thus read as values >= 2^31, i.e.
+    // out of range, skipped like any other (results for bad data unspecified).
+    auto key_ld = [&](long long e) -> long long {
+        return p.idx64 ? __ldg(static_cast<const long long*>(p.idx) + e)
+                       : (long long)(unsigned)__ldg(static_cast<const int*>(p.idx) + e);
+    };
+    const long long prevk = (e_lo > 0) ? key_ld(e_lo - 1) : KEY_BEFORE;
+    const long long nextk = (e_hi < p.E) ? key_ld(e_hi) : KEY_AFTER;
+    const long long first_key = (nrows > 0) ? key_ld(e_lo) : KEY_AFTER;
 
     auto vec_col = [&](int j) { return li + j * LPR; };
     auto write_row = [&](long long key, const float (&acc)[VPL][VW], long long count) {
@@ -538,14 +548,8 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
             const long long r_base = e_lo + (long long)s * RS;
             int cnt = (int)(e_hi - r_base);
             cnt = cnt < 0 ? 0 : (cnt > RS ? RS : cnt);
-            // int32 keys sit in the low half of 8-byte slots: sign-extend them, so
-            // they compare equal to the load_index() copies (prevk / nextk) — a
-            // zero-extended negative key would break the carry chain's consistency
-            auto slot_key = [&](int i) -> long long {
-                return isz == 4 ? (long long)(int)(unsigned)gkey[i] : gkey[i];
-            };
-            const long long kmine = (li < cnt) ? slot_key(li) : KEY_AFTER;
-            const long long kprev = (li == 0) ? cur : ((li <= cnt) ? slot_key(li - 1) : KEY_AFTER);
+            const long long kmine = (li < cnt) ? gkey[li] : KEY_AFTER;
+            const long long kprev = (li == 0) ? cur : ((li <= cnt) ? gkey[li - 1] : KEY_AFTER);
             float wmine = 1.0f;
             if constexpr (MODE == 2) wmine = (li < cnt) ? wring[(b * G + gi) * RS + li] : 0.0f;
             // is_seg of the whole stage (Alg. 1): row r starts a segment iff its
@@ -601,7 +605,7 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
                     nxt[r][j] = (r < c && col_ok[j])
                                     ? ld_stream(reinterpret_cast<const Raw*>(base + (long long)r * F + vec_col(j) * VW))
                                     : Raw{};
-            nkey = (li < c) ? load_index(p.idx, p.idx64, rb + li) : KEY_AFTER;
+            nkey = (li < c) ? key_ld(rb + li) : KEY_AFTER;
         };
         if (nst_w > 0) fetch(0);
 #pragma unroll 1
