@@ -1,5 +1,4 @@
-timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "bad_data or stream or int64" 2>&1 | tail -2
-for i in 1 2; do
-(cd abold && python bench.py --no-cpu-baseline 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('OLD', d['value'], d['roofline']['kernel_ms'])")
-python bench.py --no-cpu-baseline 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('NEW', d['value'], d['roofline']['kernel_ms'])"
-done
+bash tools/gpu_round.sh r1g
+timeout 900 python tools/report_configs.py --md gpurun_out/r1g_configs.md --jsonl gpurun_out/r1g_configs.jsonl > gpurun_out/r1g_configs.log 2>&1; echo "configs rc=$?"
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r1g_smoke.log 2>&1; echo "smoke rc=$?"; tail -1 gpurun_out/r1g_smoke.log
+du -sh gpurun_out
