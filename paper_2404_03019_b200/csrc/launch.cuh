@@ -218,6 +218,11 @@ cudaError_t launch_stream_gather(const StreamParams& p, const EdgeTileParams& fi
     GEOT_GSHAPE(4, 16, 4, 4)
     GEOT_GSHAPE(8, 16, 6, 4)
     GEOT_GSHAPE(16, 16, 6, 4)
+    GEOT_GSHAPE(16, 16, 8, 3)
+    GEOT_GSHAPE(16, 16, 12, 2)
+    GEOT_GSHAPE(8, 16, 8, 3)
+    GEOT_GSHAPE(32, 16, 8, 3)
+    GEOT_GSHAPE(32, 16, 12, 2)
     GEOT_GSHAPE(32, 16, 6, 4)
 #undef GEOT_GSHAPE_I
 #undef GEOT_GSHAPE

@@ -356,7 +356,8 @@ def test_fused_gather_stream_stress_and_weighted(geot, kind):
     for op in ("sum", "mean", "max"):
         L, dst, src, x = fused_case(E, S, V, F, "f32", "int", kind, 6)
         ref = oracle.gather_segment_reduce(x, src, dst, S, op, nthreads=oracle.default_threads())
-        for cfg in ({"variant": 3}, {"variant": 1}):
+        for cfg in ({"variant": 3}, {"variant": 3, "warps_per_cta": 16, "rows_per_group": 8, "stages": 3},
+                    {"variant": 3, "warps_per_cta": 16, "rows_per_group": 12, "stages": 2}, {"variant": 1}):
             y = geot.geot_gather_segment_reduce(torch.from_numpy(x).cuda(), torch.from_numpy(src).cuda(),
                                                 torch.from_numpy(dst).cuda(), S, op, cfg=cfg)
             check(y.cpu().numpy(), ref, op, "f32", "int", counts=L, what=f"gather-stream {kind} {op} {cfg}")

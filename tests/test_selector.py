@@ -79,12 +79,14 @@ def test_select_config_always_valid(L):
                         wide = 4 if dt == 0 else 8
                         if c.variant == 3:  # 16-byte lane vectors, 8/16/32 lanes per row
                             assert c.vec_elems == wide and c.lanes_per_row >= 4
-                            rs_def = min(6, c.lanes_per_row)
+                            lpr = c.lanes_per_row
+                            fused_pipes = {(16, min(6, lpr), 4)} | ({(16, 8, 3)} if lpr >= 8 else set()) | \
+                                ({(16, 12, 2)} if lpr >= 16 else set())
                             assert not fused or (c.vecs_per_lane == 1 and (c.warps_per_cta, c.rows_per_group, c.stages)
-                                                 == (16, rs_def, 4))
+                                                 in fused_pipes)
                             assert F // wide <= c.lanes_per_row * c.vecs_per_lane
                             pipes = STREAM_PIPES_LPR4 if c.lanes_per_row == 4 else STREAM_PIPES[c.vecs_per_lane]
-                            assert (c.warps_per_cta, c.rows_per_group, c.stages) in pipes
+                            assert fused or (c.warps_per_cta, c.rows_per_group, c.stages) in pipes
                         elif c.variant == 2:
                             assert not fused and (F in (1, 2, 4, 8) or (dt == 1 and F == 16))
                         else:

@@ -106,8 +106,9 @@ def candidate_configs(E, S, F, dtype, fused, quick=False):
         out.append({"variant": 2})
     if stream_ok:
         pipes = [(16, 4, 4), (8, 4, 8), (8, 4, 1)] if shape[0] == 4 else STREAM_PIPES[shape[1]]
-        if fused:  # the gather form: one pipeline per lane shape (launch.cuh)
-            pipes = [(16, min(6, shape[0]), 4)]
+        if fused:  # the gather form's compiled pipelines (launch.cuh launch_stream_gather)
+            pipes = [(16, min(6, shape[0]), 4)] + ([(16, 8, 3)] if shape[0] >= 8 else []) + \
+                ([(16, 12, 2)] if shape[0] >= 16 else [])
         for (w, rs, ns) in pipes:
             if rs <= shape[0]:
                 out.append({"variant": 3, "warps_per_cta": w, "rows_per_group": rs, "stages": ns})
@@ -175,6 +176,11 @@ def selector_grid():
     for F in (16, 32, 64, 128):
         for avg in (8, 64, 492):
             g.append((1 << 23, (1 << 23) // avg, F, "f32", "powerlaw", "sum", True))
+    for F in (64, 128):
+        for avg in (8, 64):
+            g.append((1 << 23, (1 << 23) // avg, F, "bf16", "powerlaw", "sum", True))
+    for avg in (16, 492):
+        g.append((1 << 25, (1 << 25) // avg, 64, "f32", "powerlaw", "sum", True))
     # small graphs (Cora/Citeseer/PubMed-sized) and arxiv-sized ones
     for F in (8, 16, 32, 64, 128):
         for E in (4096, 10_556, 40_000):
