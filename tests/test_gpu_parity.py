@@ -146,15 +146,15 @@ def test_stream_variant(geot, F, dtype, op):
 # every compiled pipeline (W warps, RS rows per stage, NS stages; NS=1 is the
 # LDG register pipeline) of every lane shape (LPR 4/8/16/32, VPL 1..8)
 PIPES = {4: [(16, 4, 4), (8, 4, 8), (8, 4, 1)],
-         1: [(16, 6, 4), (8, 6, 8), (16, 3, 8), (8, 8, 6), (8, 4, 1), (8, 8, 1)],
+         1: [(16, 6, 4), (8, 6, 8), (16, 3, 8), (8, 8, 6), (8, 4, 1), (8, 8, 1), (16, 12, 2), (16, 8, 3)],
          2: [(16, 3, 4), (8, 3, 8), (8, 4, 1)], 4.5: [(8, 3, 4), (8, 2, 1)], 8: [(8, 1, 4), (8, 1, 6), (8, 1, 1)]}
 
 
 @pytest.mark.parametrize("F,key", [(16, 4), (32, 1), (64, 1), (128, 1), (256, 2), (512, 4.5), (1024, 8)])
 def test_stream_every_pipeline(geot, F, key):
     for (w, rs, ns) in PIPES[key]:
-        if rs > max(4, min(32, F // 4)):
-            continue
+        if rs > max(4, min(32, F // 4)) or ((w, rs, ns) in ((16, 12, 2), (16, 8, 3)) and F != 64):
+            continue  # (the deeper 16-warp pipelines are compiled for 256-byte rows only)
         cfg = {"variant": STREAM, "warps_per_cta": w, "rows_per_group": rs, "stages": ns}
         for op in ("sum", "max"):
             parity(geot, 90_001, 9_000, F, op, "f32", "int", "powerlaw15", seed=F + w + rs + ns, cfg=cfg)
