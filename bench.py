@@ -1,20 +1,25 @@
 """bench.py — GeoT segment-reduction throughput on B200 (the driver's contract).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--workload arxiv]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+                    [--workload products|arxiv|reddit|sweep|cora] [--F F] [--dist D] [--op OP] [--weighted]
 
 Metric (BASELINE.json): segment_reduce achieved HBM GB/s and % of B200 peak;
-edges*F/s at 1/2/4/8 GPUs.  Workload at N=1: configs[1], the ogbn-arxiv-shaped
-graph (169,343 segments, 1,166,243 sorted edges, Lomax(2) degree mix,
-F=128 fp32, sum).  A step = one geot_segment_reduce call (H1 features + H2
-selection on the host, H4-H7 + H5 carries on the device) over the resident
-inputs.  Bytes = src rows read + indices + out rows written.
-For N>1 (torchrun, one rank per GPU) the global graph is N times larger,
-partitioned at segment boundaries by geot_partition (H9) once per graph, and
-every rank reduces its own shard with no data-path collective (weak scaling);
-value = all ranks' bytes / max-over-ranks time.
+edges*F/s at 1/2/4/8 GPUs.  Default workload: BASELINE.json configs[3], the
+ogbn-products-shaped graph (2,449,029 segments, 61,859,140 sorted edges,
+Lomax(2) degree mix, F=128, bf16 values, sum) — the configuration the metric's
+"at 1/2/4/8 GPUs" names and the largest single-GPU segment_reduce config.
+A step = one geot_segment_reduce call (H1 features + H2 selection on the host,
+H4-H7 + H5 carries on the device) over inputs resident in HBM.
+Bytes = src rows read + indices + out rows written.
 
---impl reference times the CPU oracle (oracle/, fp64) on the host cores on the
-same workload (rank 0 only), as the reference arm for this tier.
+N > 1 (torchrun, one rank per GPU): STRONG scaling of the same global graph.
+Every rank builds the global index, runs geot_partition (H9, once per graph)
+and reduces only its own shard [e_p, e_{p+1}) -> rows [s_p, s_{p+1}) with
+seg_base = s_p; no data-path collective (NCCL carries the barrier and the
+max-over-ranks time only).  value = global bytes / max-over-ranks time.
+
+--impl reference times the CPU oracle (oracle/, fp64) on the host cores, rank
+0 only, on a bounded sample (the leading segments) of the same workload.
 """
 from __future__ import annotations
 
@@ -46,10 +51,11 @@ def dist_env():
     return ws, rank, local
 
 
-def algorithmic_bytes(E, S, F, esz, isz, fused=False):
-    """src rows read + indices + out rows written."""
+def algorithmic_bytes(E, S, F, esz, isz, fused=False, weighted=False):
+    """src rows read + indices + out rows written (fused: the
+    logical gathered rows, both indices, and the weights when weighted)."""
     if fused:
-        return E * F * esz + 2 * E * isz + S * F * esz
+        return E * F * esz + 2 * E * isz + S * F * esz + (4 * E if weighted else 0)
     return E * F * esz + E * isz + S * F * esz
 
 
@@ -62,6 +68,19 @@ def peaks():
         except Exception:
             pass
     return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def l2_gather_peak():
+    """Measured ceiling of L2-resident random 256-byte row gathers (tools/microbench/
+    l2_gather.cu, written by tools/l2_gather_peak.py into profiles/)."""
+    p = os.path.join(ROOT, "profiles", "l2_gather_peak.json")
+    if os.path.exists(p):
+        try:
+            d = json.load(open(p))
+            return float(d["gbs"]), f"measured (profiles/l2_gather_peak.json, {d.get('how', '')})"
+        except Exception:
+            pass
+    return None, None
 
 
 _SAMPLER_SRC = r"""
@@ -93,7 +112,7 @@ class ClockSampler:
                0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
                0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
 
-    def __init__(self, index, period=float(os.environ.get("GEOT_CLOCK_PERIOD", "0.005"))):
+    def __init__(self, index, period=float(os.environ.get("GEOT_CLOCK_PERIOD", "0.002"))):
         self.index, self.period = index, period
         self.samples, self.reasons, self.max_mhz, self.err = [], set(), None, ""
         self.proc = None
@@ -128,32 +147,101 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-def host_workload(w, e_chunk=1 << 17):
-    """Host copy of the workload for the oracle (host generator only)."""
+def make_workload(args):
+    over = {}
+    if args.F:
+        over["F"] = args.F
+    if args.dist:
+        over["dist"] = args.dist
+    w = synth.workload(args.workload, **over)
+    w["op"] = args.op
+    w["fused"] = "V" in w
+    w["weighted"] = bool(args.weighted) and w["fused"]
+    if w["weighted"] and args.op != "sum":
+        raise SystemExit("--weighted is the sum-only SpMM form (P:330)")
+    return w
+
+
+def mode_of(op):
+    return "signed" if op == "max" else "real"
+
+
+def workload_config(w, N, e_rank_max=None):
+    c = {"workload": f"{w['name']}-shaped", "E": w["E"], "S": w["S"], "F": w["F"], "op": w["op"],
+         "value_dtype": w["dtype"], "index": "int32",
+         "degree_dist": f"{'Lomax(alpha=2)' if w['dist'] == 'powerlaw' else 'uniform'} segment lengths",
+         "seed": w["seed"],
+         "parallelism": (f"{N} segment-range shards of one graph (geot_partition), no data-path collective"
+                         if N > 1 else "1 GPU"),
+         "l2": "inputs larger than L2 (no flush needed)"}
+    if w["fused"]:
+        c["form"] = "fused gather (index_weight_segment_reduce)" if w["weighted"] else \
+            "fused gather (index_segment_reduce)"
+        c["V"] = w["V"]
+        c["l2"] = "x (the gathered rows) is L2-resident by design; index streams larger than L2 (no flush)"
+    if e_rank_max is not None:
+        c["edges_per_rank_max"] = int(e_rank_max)
+    return c
+
+
+def leading_sample(L, max_edges):
+    """The leading segments of the graph holding at most max_edges edges (>= 1 segment)."""
+    b = synth.lengths_to_bounds(L)
+    k = int(np.searchsorted(b, max_edges, side="right") - 1)
+    k = max(1, min(k, L.shape[0]))
+    return k, int(b[k])
+
+
+def host_sample(w, max_edges, e_chunk=1 << 17):
+    """Host copy of the leading segments of the workload (host generator only)."""
     L = synth.segment_lengths(w["E"], w["S"], w["dist"], w["seed"])
-    idx = synth.lengths_to_index(L, "i32")
-    X = np.empty((w["E"], w["F"]), dtype=np.float32 if w["dtype"] == "f32" else np.uint16)
-    for e0 in range(0, w["E"], e_chunk):
-        n = min(e_chunk, w["E"] - e0)
-        X[e0:e0 + n] = synth.values(w["seed"], e0, n, w["F"], w["dtype"], "real")
-    return L, idx, X
+    k, Es = leading_sample(L, max_edges)
+    idx = synth.lengths_to_index(L[:k], "i32")
+    mode = mode_of(w["op"])
+    if w["fused"]:
+        x = np.empty((w["V"], w["F"]), dtype=np.float32 if w["dtype"] == "f32" else np.uint16)
+        for r0 in range(0, w["V"], e_chunk):
+            n = min(e_chunk, w["V"] - r0)
+            x[r0:r0 + n] = synth.values(w["seed"], r0, n, w["F"], w["dtype"], mode)
+        src = synth.src_index(w["seed2"], 0, Es, w["V"]).astype(np.int32)
+        wt = synth.weights(w["seed3"], 0, Es) if w["weighted"] else None
+        return k, Es, idx, (x, src, wt)
+    X = np.empty((Es, w["F"]), dtype=np.float32 if w["dtype"] == "f32" else np.uint16)
+    for e0 in range(0, Es, e_chunk):
+        n = min(e_chunk, Es - e0)
+        X[e0:e0 + n] = synth.values(w["seed"], e0, n, w["F"], w["dtype"], mode)
+    return k, Es, idx, X
 
 
-def cpu_oracle_time(w, budget_s=10.0, op="sum"):
-    """Time the oracle as it stands on the host cores, on the full workload,
-    repeated until ~budget_s of CPU work.  Returns (GB/s, cores, sample, per-run s)."""
+def run_oracle(w, k, idx, data, cores):
     import oracle
-    L, idx, X = host_workload(w)
+    if w["fused"]:
+        x, src, wt = data
+        return oracle.gather_segment_reduce(x, src, idx, k, w["op"], weight=wt, nthreads=cores)
+    return oracle.segment_reduce(data, idx, k, w["op"], nthreads=cores)
+
+
+def sample_bytes(w, k, Es):
+    esz = 4 if w["dtype"] == "f32" else 2
+    return algorithmic_bytes(Es, k, w["F"], esz, 4, w["fused"], w["weighted"])
+
+
+def cpu_oracle_time(w, k, Es, idx, data, budget_s):
+    """The oracle as it stands, on the host cores, on a sample (the leading k
+    segments, Es edges), repeated until ~budget_s of CPU work."""
+    import oracle
     cores = oracle.default_threads()
-    B = algorithmic_bytes(w["E"], w["S"], w["F"], 4 if w["dtype"] == "f32" else 2, 4)
+    B = sample_bytes(w, k, Es)
     times = []
     t_all = time.perf_counter()
     while not times or (time.perf_counter() - t_all < budget_s and len(times) < 50):
         t0 = time.perf_counter()
-        oracle.segment_reduce(X, idx, w["S"], op, nthreads=cores)
+        run_oracle(w, k, idx, data, cores)
         times.append(time.perf_counter() - t0)
     t = statistics.median(times)
-    return B / t / 1e9, cores, f"full {w['name']}-shaped problem, {len(times)} oracle runs (median)", t
+    sample = (f"leading {k:,} segments / {Es:,} edges ({B / 1e9:.2f} GB algorithmic) of the {w['name']}-shaped "
+              f"workload, fp64 C oracle on {cores} threads, median of {len(times)} runs")
+    return B / t / 1e9, cores, sample
 
 
 # ----------------------------------------------------------------------------- reference arm
@@ -161,36 +249,30 @@ def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
-    w = synth.workload(args.workload)
+    w = make_workload(args)
     import oracle
-    L, idx, X = host_workload(w)
     cores = oracle.default_threads()
-    B = algorithmic_bytes(w["E"], w["S"], w["F"], 4 if w["dtype"] == "f32" else 2, 4)
+    k, Es, idx, data = host_sample(w, args.ref_sample_edges)
+    B = sample_bytes(w, k, Es)
     for _ in range(args.warmup):
-        oracle.segment_reduce(X, idx, w["S"], "sum", nthreads=cores)
+        run_oracle(w, k, idx, data, cores)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        oracle.segment_reduce(X, idx, w["S"], "sum", nthreads=cores)
+        run_oracle(w, k, idx, data, cores)
     dt = (time.perf_counter() - t0) / args.steps
     v = B / dt / 1e9
+    sample = (f"leading {k:,} segments / {Es:,} edges ({B / 1e9:.3f} GB algorithmic) of the {w['name']}-shaped "
+              f"workload per step (fp64 C oracle, {cores} threads)")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(w, 1),
-        "cpu_baseline": {"value": round(v, 3), "unit": UNIT, "cores": cores, "kind": "oracle",
-                         "sample": f"full {w['name']}-shaped problem per step (fp64 C oracle, {cores} threads)"},
+        "cpu_baseline": {"value": round(v, 3), "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
         "e2e": {"value": round(v, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
-
-
-def workload_config(w, N):
-    return {"workload": f"{w['name']}-shaped", "E": w["E"] * N, "S": w["S"] * N, "F": w["F"], "op": "sum",
-            "value_dtype": w["dtype"], "index": "int32", "degree_dist": "Lomax(alpha=2) segment lengths",
-            "seed": w["seed"], "parallelism": f"{N} segment-range shard(s), no data-path collective",
-            "l2": "inputs larger than L2 (no flush needed)"}
 
 
 # ----------------------------------------------------------------------------- our arm
@@ -208,41 +290,53 @@ def run_ours(args):
     import synth.device as sd
     from paper_2404_03019_b200 import _lib, shard
 
-    w = synth.workload(args.workload)
-    Eg, Sg, F = w["E"] * N, w["S"] * N, w["F"]
+    w = make_workload(args)
+    Eg, Sg, F, op = w["E"], w["S"], w["F"], w["op"]
     tdt = torch.float32 if w["dtype"] == "f32" else torch.bfloat16
     esz = 4 if w["dtype"] == "f32" else 2
-    # ---- global index (same on every rank), partition once per graph (H9)
+    mode = mode_of(op)
+    # ---- global index (identical on every rank); partition once per graph (H9)
     L = synth.segment_lengths(Eg, Sg, w["dist"], w["seed"])
     bounds = torch.from_numpy(synth.lengths_to_bounds(L)).to(dev)
-    if N > 1:
-        gidx = sd.expand_index(bounds, 0, Eg, torch.int32)
-        sb, eb = [b.cpu().numpy() for b in geot.geot_partition(gidx, Sg, N)]
-        e0, e1, s0, s1 = shard.shard_of(sb, eb, rank)
-        idx = gidx[e0:e1].clone()
-        del gidx
-    else:
-        e0, e1, s0, s1 = 0, Eg, 0, Sg
-        idx = sd.expand_index(bounds, 0, Eg, torch.int32)
+    gidx = sd.expand_index(bounds, 0, Eg, torch.int32)
+    sb_t, eb_t = geot.geot_partition(gidx, Sg, N)
+    sb, eb = sb_t.cpu().numpy(), eb_t.cpu().numpy()
+    e0, e1, s0, s1 = shard.shard_of(sb, eb, rank)
     E, S = e1 - e0, s1 - s0
-    X = sd.values(E, F, w["seed"], e_begin=e0, dtype=tdt, mode="real", device=dev)
+    idx = gidx[e0:e1].clone() if N > 1 else gidx
+    del gidx
+    if w["fused"]:  # x replicated on every rank; src (and weights) sliced like dst
+        V = w["V"]
+        x = sd.values(V, F, w["seed"], dtype=tdt, mode=mode, device=dev)
+        src = sd.src_index(E, V, w["seed2"], e_begin=e0, device=dev)
+        wt = sd.values(E, 1, w["seed3"], e_begin=e0, dtype=torch.float32, device=dev)[:, 0].contiguous() \
+            if w["weighted"] else None
+    else:
+        X = sd.values(E, F, w["seed"], e_begin=e0, dtype=tdt, mode=mode, device=dev)
     out = torch.empty((S, F), dtype=tdt, device=dev)
-    B_rank = algorithmic_bytes(E, S, F, esz, 4)
-    cfg = geot.geot_select_config(E, S, F, "sum", tdt, torch.int32, False)
+    B_rank = algorithmic_bytes(E, S, F, esz, 4, w["fused"], w["weighted"])
+    cfg = geot.geot_select_config(E, S, F, op, tdt, torch.int32, w["fused"])
     user_cfg = json.loads(args.cfg) if args.cfg else None  # experiments only (selector override)
     if user_cfg:
-        for k, v in user_cfg.items():
-            setattr(cfg, k, int(v))
+        for k_, v_ in user_cfg.items():
+            setattr(cfg, k_, int(v_))
     stream = torch.cuda.current_stream(dev)
 
     L_ = _lib.load()
     prof = getattr(L_, "geot_profile_events", None)
-    if prof is not None:
-        prof.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
-        prof.restype = None
 
-    def step():
-        geot.geot_segment_reduce(X, idx, S, "sum", out=out, seg_base=s0, cfg=user_cfg)
+    if w["fused"]:
+        def call(xx, ss, ii, ww):
+            geot.geot_gather_segment_reduce(xx, ss, ii, S, op, weight=ww, out=out, seg_base=s0, cfg=user_cfg)
+
+        def step():
+            call(x, src, idx, wt)
+    else:
+        def call(xx, ii):
+            geot.geot_segment_reduce(xx, ii, S, op, out=out, seg_base=s0, cfg=user_cfg)
+
+        def step():
+            call(X, idx)
 
     def barrier():
         if N > 1:
@@ -257,6 +351,7 @@ def run_ours(args):
         a.record(stream)
         b.record(stream)
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
     launches0 = geot.geot_launch_count()
@@ -271,15 +366,14 @@ def run_ours(args):
     barrier()
     launches = geot.geot_launch_count() - launches0
     ms = t_start.elapsed_time(t_end) / args.steps
-    kern_ms = None
-    if prof is not None:
-        kern_ms = statistics.mean(a.elapsed_time(b) for a, b in kev)
+    kern_ms = statistics.mean(a.elapsed_time(b) for a, b in kev) if prof is not None else None
     t = [ms, kern_ms if kern_ms is not None else ms]
     if N > 1:
         t = shard.max_over_ranks(t)
-        B_all, EF_all = shard.sum_over_ranks([B_rank, E * F])
+        B_all, EF_all, E_max = shard.sum_over_ranks([B_rank, E * F, 0])[0], float(Eg * F), \
+            shard.max_over_ranks([E])[0]
     else:
-        B_all, EF_all = float(B_rank), float(E * F)
+        B_all, EF_all, E_max = float(B_rank), float(E * F), E
     ms, kern_ms_max = float(t[0]), float(t[1])
     ag_ms = None
     if N > 1 and args.allgather:  # optional output all-gather (COLL-0), timed separately
@@ -297,19 +391,32 @@ def run_ours(args):
     value = B_all / (ms * 1e-3) / 1e9
     peak, peak_src = peaks()
 
-    # ---- end-to-end through the public API with host buffers (pinned), N ranks
+    # ---- end-to-end through the public API with host buffers (pinned), N ranks:
+    # every step copies its inputs host->device, reduces, and reads the result back
     k_e2e = max(1, min(args.steps, args.e2e_steps))
-    hX = torch.empty((E, F), dtype=tdt, pin_memory=True)
-    hX.copy_(X)
-    hidx = torch.empty(E, dtype=torch.int32, pin_memory=True)
-    hidx.copy_(idx)
+
+    def pinned_like(t_):
+        try:
+            h = torch.empty(t_.shape, dtype=t_.dtype, pin_memory=True)
+        except RuntimeError:  # pinning refused (host memory limits): pageable staging
+            h = torch.empty(t_.shape, dtype=t_.dtype)
+        h.copy_(t_)
+        return h
+
+    if w["fused"]:
+        h_in = [pinned_like(x), pinned_like(src), pinned_like(idx)] + ([pinned_like(wt)] if w["weighted"] else [])
+    else:
+        h_in = [pinned_like(X), pinned_like(idx)]
+    d_in = [torch.empty_like(h, device=dev) for h in h_in]
     hout = torch.empty((S, F), dtype=tdt, pin_memory=True)
-    dX, didx = torch.empty_like(X), torch.empty_like(idx)
 
     def e2e_step():
-        dX.copy_(hX, non_blocking=True)
-        didx.copy_(hidx, non_blocking=True)
-        geot.geot_segment_reduce(dX, didx, S, "sum", out=out, seg_base=s0)
+        for h, d in zip(h_in, d_in):
+            d.copy_(h, non_blocking=True)
+        if w["fused"]:
+            call(d_in[0], d_in[1], d_in[2], d_in[3] if w["weighted"] else None)
+        else:
+            call(d_in[0], d_in[1])
         hout.copy_(out, non_blocking=True)
 
     e2e_step()
@@ -321,13 +428,12 @@ def run_ours(args):
         e2e_step()
     eb_.record(stream)
     torch.cuda.synchronize()
-    te = torch.tensor([ea.elapsed_time(eb_) / k_e2e], dtype=torch.float64, device=dev)
+    e2e_ms = ea.elapsed_time(eb_) / k_e2e
     if N > 1:
-        torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
-    e2e_ms = float(te[0])
-    h2d = E * F * esz + E * 4
+        e2e_ms = shard.max_over_ranks([e2e_ms])[0]
+    h2d = sum(h.numel() * h.element_size() for h in h_in)
     d2h = S * F * esz
-    del hX, dX, didx
+    del h_in, d_in
 
     if rank != 0:
         if N > 1:
@@ -335,26 +441,35 @@ def run_ours(args):
         return 0
 
     kern_bytes = B_rank  # per launch of the dominant kernel on rank 0's shard
-    achieved = kern_bytes / (kern_ms_max * 1e-3) / 1e9 if kern_ms is not None else value / N
+    achieved = kern_bytes / (kern_ms_max * 1e-3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
+    tkey = f"{w['name']}:F{F}:{w['dtype']}:{op}:{w['dist']}" + (":w" if w["weighted"] else "")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(f"{w['name']}:{N}") or json.load(open(tp)).get(w["name"])
+            d = json.load(open(tp))
+            traffic = d.get(f"{tkey}:N{N}") or (d.get(tkey) if N == 1 else None)
         except Exception:
             traffic = None
+    kname = {1: "edge_tile_kernel (+ carry_fixup_kernel)", 2: "narrow_kernel", 3: "stream_kernel"}.get(cfg.variant, "?")
+    if w["fused"]:
+        hbm_min = V * F * esz + (2 * E) * 4 + S * F * esz + (4 * E if w["weighted"] else 0)
+        l2p, l2src = l2_gather_peak()
+        roof = {"bound": "l2_gather", "achieved": round(achieved, 1), "peak": l2p, "unit": "GB/s",
+                "frac": round(achieved / l2p, 4) if l2p else None, "traffic": traffic, "peak_source": l2src,
+                "hbm_min_bytes_per_launch": hbm_min,
+                "hbm_min_frac": round(hbm_min / (kern_ms_max * 1e-3) / 1e9 / peak, 4)}
+    else:
+        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src}
+    roof.update({"kernel": kname, "kernel_ms": round(kern_ms_max, 5), "algorithmic_bytes_per_launch": kern_bytes})
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": N, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": w["dtype"], "data": "synthetic",
-        "config": workload_config(w, N),
+        "config": workload_config(w, N, E_max if N > 1 else None),
         "pct_of_peak": round(100 * value / (N * peak), 2), "edges_F_per_s": EF_all / (ms * 1e-3),
-        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
-                     "kernel": {1: "edge_tile_kernel (+ carry_fixup_kernel)", 2: "narrow_kernel",
-                                3: "stream_kernel"}.get(cfg.variant, "?"),
-                     "kernel_ms": round(kern_ms_max, 5) if kern_ms is not None else None,
-                     "algorithmic_bytes_per_launch": kern_bytes},
+        "roofline": roof,
         "e2e": {"value": round(B_all / (e2e_ms * 1e-3) / 1e9, 3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "steps": k_e2e, "ms_per_step": round(e2e_ms, 4)},
         "gpu_launches": int(launches),
@@ -363,7 +478,14 @@ def run_ours(args):
         "allgather_ms": ag_ms,
     }
     if N == 1 and not args.no_cpu_baseline:
-        v, cores, sample, _ = cpu_oracle_time(w, budget_s=args.cpu_budget)
+        # bounded sample: the leading segments, copied from the device-resident inputs
+        k, Es = leading_sample(L, args.cpu_sample_edges)
+        hidx = idx[:Es].cpu().numpy()
+        if w["fused"]:
+            data = (_host_vals(x), src[:Es].cpu().numpy(), wt[:Es].cpu().numpy() if w["weighted"] else None)
+        else:
+            data = _host_vals(X[:Es])
+        v, cores, sample = cpu_oracle_time(w, k, Es, hidx, data, args.cpu_budget)
         line["cpu_baseline"] = {"value": round(v, 3), "unit": UNIT, "cores": cores, "kind": "oracle",
                                 "sample": sample}
     print(json.dumps(line), flush=True)
@@ -372,15 +494,29 @@ def run_ours(args):
     return 0
 
 
+def _host_vals(t):
+    import torch
+    t = t.cpu()
+    if t.dtype == torch.bfloat16:
+        return t.view(torch.int16).numpy().view(np.uint16)
+    return t.numpy()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="arxiv", choices=sorted(synth.WORKLOADS))
-    ap.add_argument("--e2e-steps", type=int, default=10)
-    ap.add_argument("--cpu-budget", type=float, default=8.0)
+    ap.add_argument("--workload", default="products", choices=sorted(synth.WORKLOADS))
+    ap.add_argument("--F", type=int, default=0, help="feature width override (the width/skew sweep)")
+    ap.add_argument("--dist", default="", choices=["", "powerlaw", "uniform"], help="segment-length distribution")
+    ap.add_argument("--op", default="sum", choices=["sum", "mean", "max"])
+    ap.add_argument("--weighted", action="store_true", help="fused workloads: index_weight_segment_reduce (P:330)")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--cpu-budget", type=float, default=10.0)
+    ap.add_argument("--cpu-sample-edges", type=int, default=4_000_000)
+    ap.add_argument("--ref-sample-edges", type=int, default=1_000_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cfg", default="", help="JSON geot_config override (experiments; default = the selector)")
     ap.add_argument("--allgather", action="store_true", help="N>1: also time the optional output all-gather")

@@ -28,40 +28,63 @@ BAD_UNSORTED, BAD_IDX_RANGE, BAD_SRC_RANGE = 1, 2, 4
 _lib = None
 
 
-def build(force: bool = False) -> str:
-    """gcc -O2 (no -ffast-math) the oracle into oracle/libgeot_oracle.so."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        tmp = _LIB + f".tmp{os.getpid()}"
+def build(force: bool = False, src: str = _SRC, out: str = _LIB) -> str:
+    """gcc -O2 (no -ffast-math) the oracle into oracle/libgeot_oracle.so.
+    (`src`/`out` other than the defaults: the mutation tests build deliberately
+    broken copies to show that the pins catch them.)"""
+    if force or not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(src):
+        tmp = out + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", "-O2", "-std=gnu11", "-fPIC", "-shared", "-fno-fast-math",
-                               "-o", tmp, _SRC, "-lpthread", "-lm"])
-        os.replace(tmp, _LIB)
-    return _LIB
+                               "-o", tmp, src, "-lpthread", "-lm"])
+        os.replace(tmp, out)
+    return out
+
+
+def _load(path):
+    L = ctypes.CDLL(path)
+    vp, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
+    L.oracle_validate.argtypes = [vp, i32, i64, i64, vp, i64]
+    L.oracle_validate.restype = i32
+    L.oracle_offsets.argtypes = [vp, i32, i64, i64, vp]
+    L.oracle_offsets.restype = None
+    L.oracle_segment_reduce.argtypes = [vp, i32, vp, i32, i64, i64, i64, i32, vp, vp, vp, i32]
+    L.oracle_segment_reduce.restype = i32
+    L.oracle_gather_segment_reduce.argtypes = [vp, i32, i64, vp, vp, i32, vp, i64, i64, i64, i32,
+                                               vp, vp, vp, i32]
+    L.oracle_gather_segment_reduce.restype = i32
+    L.oracle_partition.argtypes = [vp, i32, i64, i64, i32, vp, vp]
+    L.oracle_partition.restype = i32
+    L.oracle_segment_reduce_backward.argtypes = [vp, vp, i32, vp, i32, i64, i64, i64, i32, vp]
+    L.oracle_segment_reduce_backward.restype = i32
+    L.oracle_gather_segment_reduce_backward.argtypes = [vp, vp, i64, vp, vp, i32, vp, i64, i64, i64, i32, vp,
+                                                        vp]
+    L.oracle_gather_segment_reduce_backward.restype = i32
+    return L
 
 
 def lib():
     global _lib
     if _lib is None:
         build()
-        L = ctypes.CDLL(_LIB)
-        vp, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
-        L.oracle_validate.argtypes = [vp, i32, i64, i64, vp, i64]
-        L.oracle_validate.restype = i32
-        L.oracle_offsets.argtypes = [vp, i32, i64, i64, vp]
-        L.oracle_offsets.restype = None
-        L.oracle_segment_reduce.argtypes = [vp, i32, vp, i32, i64, i64, i64, i32, vp, vp, vp, i32]
-        L.oracle_segment_reduce.restype = i32
-        L.oracle_gather_segment_reduce.argtypes = [vp, i32, i64, vp, vp, i32, vp, i64, i64, i64, i32,
-                                                   vp, vp, vp, i32]
-        L.oracle_gather_segment_reduce.restype = i32
-        L.oracle_partition.argtypes = [vp, i32, i64, i64, i32, vp, vp]
-        L.oracle_partition.restype = i32
-        L.oracle_segment_reduce_backward.argtypes = [vp, vp, i32, vp, i32, i64, i64, i64, i32, vp]
-        L.oracle_segment_reduce_backward.restype = i32
-        L.oracle_gather_segment_reduce_backward.argtypes = [vp, vp, i64, vp, vp, i32, vp, i64, i64, i64, i32, vp,
-                                                            vp]
-        L.oracle_gather_segment_reduce_backward.restype = i32
-        _lib = L
+        _lib = _load(_LIB)
     return _lib
+
+
+class use_library:
+    """Context manager: route every oracle call through another build of the
+    C source (mutation tests only)."""
+
+    def __init__(self, path):
+        self.path = path
+
+    def __enter__(self):
+        global _lib
+        self.saved, _lib = lib(), _load(self.path)
+        return self
+
+    def __exit__(self, *a):
+        global _lib
+        _lib = self.saved
 
 
 def _ptr(a):

@@ -192,6 +192,8 @@ def geot_gather_segment_reduce(x, src_idx, dst_idx, num_segments=None, op="sum",
     E = dst_idx.shape[0]
     if out is None:
         out = torch.empty((S, F), dtype=x.dtype, device=dev)
+    elif out.shape != (S, F) or out.dtype != x.dtype:
+        raise ValueError("out must be [num_segments, F] with x's dtype")
     ws_n = _L.geot_workspace_size(E, S, F, _op(op), _dt(x), _it(dst_idx), 1, _cfgp(cfg))
     ws, ws_bytes = _workspace(dev, ws_n)
     with torch.cuda.device(dev):
@@ -258,6 +260,7 @@ def geot_gather_segment_reduce_backward(grad_out, x, src_idx, dst_idx, op="sum",
                                         need_x=True, need_w=False):
     """(grad_x, grad_weight) of the fused form (fp32); grad_x by fp32 atomics."""
     dev = _dev(grad_out, x, src_idx, dst_idx, weight, offsets)
+    _check_gather_backward_args(x, op, grad_out)
     S, F = grad_out.shape
     V = x.shape[0]
     E = dst_idx.numel()
@@ -271,6 +274,14 @@ def geot_gather_segment_reduce_backward(grad_out, x, src_idx, dst_idx, op="sum",
                                                           _ptr(offsets), _ptr(x), _ptr(gx), _ptr(gw), _stream(dev)),
                    "geot_gather_segment_reduce_backward")
     return gx, gw
+
+
+def _check_gather_backward_args(x, reduce, grad_out=None):
+    """The fused-form backward kernels take fp32 x / grad_out and sum/mean only."""
+    if x.dtype != torch.float32 or (grad_out is not None and grad_out.dtype != torch.float32):
+        raise TypeError("the fused-form backward supports float32 x and grad_out only")
+    if reduce not in ("sum", "mean"):
+        raise ValueError(f"the fused-form backward supports reduce='sum' or 'mean', got {reduce!r}")
 
 
 class _SegmentReduceFn(torch.autograd.Function):
@@ -312,6 +323,7 @@ def segment_reduce_autograd(idx, msg, reduce="sum", num_segments=None):
 
 def index_segment_reduce_autograd(src_idx, dst_idx, x, reduce="sum", weight=None, num_segments=None):
     """Fused form with gradients w.r.t. x (and weight): fp32, sum/mean."""
+    _check_gather_backward_args(x, reduce)  # refuse before the forward runs
     return _GatherSegmentReduceFn.apply(x, src_idx, dst_idx, weight, _num_segments(dst_idx, num_segments), reduce)
 
 

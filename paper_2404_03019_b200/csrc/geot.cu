@@ -276,7 +276,12 @@ static geot_status reduce_common(const void* X, long long V, const void* src_idx
     }
     unsigned char* wsb = static_cast<unsigned char*>(ws);
     if (c.variant == GEOT_VARIANT_NARROW) {
-        if (mode == 0 && aligned(X, 16) && aligned(idx, 16) &&
+        // narrow rows are stored whole (F * esz = 4..32 bytes, a power of two):
+        // every destination must be aligned to the row-store width
+        bool outs_row_aligned = true;
+        for (int d = 0; d < os.n; ++d)
+            outs_row_aligned = outs_row_aligned && aligned(os.ptr[d], (size_t)std::min<long long>(16, F * (long long)esz));
+        if (mode == 0 && aligned(X, 16) && aligned(idx, 16) && outs_row_aligned &&
             (it == GEOT_I64 || seg_base + S < (long long)INT_MAX)) {  // 32-bit key arithmetic
             const int nsm = sm_count();
             const WsLayout L = ws_layout(narrow_agents_max(nsm), F);
@@ -305,6 +310,10 @@ static geot_status reduce_common(const void* X, long long V, const void* src_idx
     }
     if (c.variant == GEOT_VARIANT_STREAM) {
         const int nsm = sm_count();
+        // f4 replicas launch the lane shape's default pipeline (launch.cuh): size
+        // the agents for that pipeline, not for the selected one
+        if (os.n > 1 && mode == 0) stream_default_pipe(c.lanes_per_row, c.vecs_per_lane, &c.warps_per_cta,
+                                                       &c.rows_per_group, &c.stages);
         const long long NA =
             stream_agents(nnz, c.lanes_per_row, c.warps_per_cta, nsm, c.stages == 1 ? 2 : 1);  // LDG mode: 2 CTAs/SM
         if (NA > 0) {

@@ -19,6 +19,7 @@ bool stream_eligible(long long nnz, long long F, geot_dtype dt, int fused);
 bool stream_lane_shape(long long F, geot_dtype dt, int* lpr, int* vpl);
 bool stream_pipe_compiled(int lpr, int vpl, geot_dtype dt, int w, int rs, int ns, int fused);
 bool to_stream(long long F, geot_dtype dt, geot_config* c);
+void stream_default_pipe(int lpr, int vpl, int* w, int* rs, int* ns);
 bool narrow_eligible(long long nnz, long long F, geot_dtype dt, int fused);
 
 // The generated tree itself (diagnostics / codegen-fidelity test) and its provenance.

@@ -98,8 +98,8 @@ def test_reddit_shaped_fused(geot):
 
 
 @pytest.mark.parametrize("F", [1, 4, 16, 64, 256, 1024])
-def test_sweep_widths_full(geot, F):
-    mode = "int" if F in (16, 1024) else "real"
+@pytest.mark.parametrize("mode", ["real", "int"])
+def test_sweep_widths_full(geot, F, mode):
     w, L, y = run_full(geot, "sweep", F=F, op="sum", mode=mode)
     rng = np.random.default_rng(F)
     n_random = 4000 if F <= 256 else 800

@@ -306,16 +306,24 @@ def test_rounding_to_dtype_matches_torch():
         np.testing.assert_array_equal(rb.rounded, want)
 
 
-def test_bf16_rne_ties():
-    # 1 + 2^-8 is a tie between bf16 1.0 and 1+2^-7 -> even (1.0); 1+3*2^-8 -> 1+2^-6 (even)
-    X = np.array([[1.0 + 2 ** -8], [1.0 + 3 * 2 ** -8]], dtype=np.float64)
-    # build as fp32 inputs in two singleton segments; result rounded to bf16 via bf16 input dtype
-    bits = synth.f32_to_bf16_bits(np.array([[1.0], [1.0]], np.float32))
-    r = oracle.segment_reduce(bits, np.array([0, 0]), 1, "mean")  # mean 1.0 exact
-    assert synth.bf16_bits_to_f32(r.rounded)[0, 0] == 1.0
-    import torch
-    t = torch.tensor(X[:, 0]).float().bfloat16().float().numpy()
-    assert t[0] == 1.0 and t[1] == 1.0 + 2 ** -6
+def test_bf16_rne_ties_oracle():
+    """R5: the oracle's bf16 output is round-to-nearest-EVEN of the fp32 value.
+    Segments of exactly representable bf16 inputs whose sums fall exactly on a
+    bf16 tie (or just above one), with the expected bf16 values written by hand
+    (bf16 keeps 8 significant bits: the spacing just above 1.0 is 2^-7)."""
+    vals = [[1.0], [2 ** -8],                    # seg 0: 1 + 2^-8, tie -> 1.0 (even)
+            [1.0 + 2 ** -7], [2 ** -8],          # seg 1: 1 + 3*2^-8, tie -> 1 + 2^-6 (even)
+            [1.0], [2 ** -8], [2 ** -20],        # seg 2: just above the tie -> 1 + 2^-7
+            [-1.0], [-(2 ** -8)],                # seg 3: -(1 + 2^-8), tie -> -1.0
+            [3.0], [2 ** -7]]                    # seg 4: 3 + 2^-7, tie between 3 and 3 + 2^-6 -> 3.0
+    idx = np.array([0, 0, 1, 1, 2, 2, 2, 3, 3, 4, 4])
+    bits = synth.f32_to_bf16_bits(np.array(vals, np.float32))
+    assert np.array_equal(synth.bf16_bits_to_f32(bits), np.array(vals, np.float32))  # inputs exact in bf16
+    r = oracle.segment_reduce(bits, idx, 5, "sum")
+    got = synth.bf16_bits_to_f32(r.rounded)[:, 0]
+    np.testing.assert_array_equal(got, np.array([1.0, 1.0 + 2 ** -6, 1.0 + 2 ** -7, -1.0, 3.0], np.float32))
+    np.testing.assert_array_equal(r.y64[:, 0], [1 + 2 ** -8, 1 + 3 * 2 ** -8, 1 + 2 ** -8 + 2 ** -20,
+                                                 -(1 + 2 ** -8), 3 + 2 ** -7])
 
 
 # ------------------------------------------------------------ offsets / part.
@@ -382,3 +390,94 @@ def test_exhaustive_length8_keys_group_sums():
         assert np.array_equal(r.y64[:, 0], want)
         n += 1
     assert n == 6435
+
+
+# ------------------------------------------------------- absum (tolerance A)
+# A[s,f] = sum_{e in segment s} |X[e,f]| is the denominator of every real-mode
+# sum/mean parity tolerance (R14; SURVEY.md §8(c) step 3 and the
+# "Parity rule").  It is pinned here against things other than the oracle: a
+# numpy column sum of |X|, the identity A == Y for non-negative inputs, a
+# pure-Python double loop, and the weighted/fused forms' |w * x[src]|.
+def _brute_absum(X, idx, S, src=None, w=None):
+    X = np.asarray(X, dtype=np.float64)
+    F = X.shape[1]
+    A = [[0.0] * F for _ in range(S)]
+    for s in range(S):
+        for e in range(len(idx)):
+            if int(idx[e]) != s:
+                continue
+            for f in range(F):
+                v = float(X[int(src[e]) if src is not None else e, f])
+                if w is not None:
+                    v = float(w[e]) * v
+                A[s][f] += abs(v)
+    return np.array(A, dtype=np.float64).reshape(S, F)
+
+
+def test_absum_single_segment_is_numpy_abs_column_sum():
+    """One segment among empties: A[3] = numpy |X|.sum(axis=0); empties 0."""
+    rng = np.random.default_rng(31)
+    X = (rng.random((1500, 6)) * 2 - 1).astype(np.float32)
+    idx = np.full(1500, 3)
+    for op in ("sum", "mean", "max"):  # A does not depend on the op
+        r = oracle.segment_reduce(X, idx, 7, op)
+        np.testing.assert_allclose(r.absum[3], np.abs(X.astype(np.float64)).sum(axis=0), rtol=1e-13)
+        assert np.all(r.absum[[0, 1, 2, 4, 5, 6]] == 0)
+
+
+def test_absum_equals_sum_for_nonnegative_inputs():
+    """X >= 0 => |x| = x, accumulated in the same order: A == Y64 bitwise, for
+    every segment (a missing per-segment reset would carry the previous
+    segment's total into A)."""
+    for kind in ("powerlaw", "gaps", "alternating", "singletons"):
+        L = synth.stress_lengths(kind, 4000, 300, seed=5)
+        idx = synth.lengths_to_index(L)
+        X = synth.values_f32(9, 0, 4000, 5, "f32", "real")  # U[0,1)
+        r = oracle.segment_reduce(X, idx, 300, "sum")
+        np.testing.assert_array_equal(r.absum, r.y64)
+        m = oracle.segment_reduce(X, idx, 300, "mean")
+        np.testing.assert_array_equal(m.absum, r.y64)
+
+
+def test_absum_signed_brute_force():
+    """Signed values, random sorted index with empty segments: A equals the
+    Python double loop (same fp64 ascending-e order => bitwise)."""
+    rng = np.random.default_rng(32)
+    for trial in range(60):
+        E, S, F = int(rng.integers(0, 50)), int(rng.integers(1, 10)), int(rng.integers(1, 4))
+        idx = np.sort(rng.integers(0, S, size=E))
+        X = (rng.random((E, F)) * 2 - 1).astype(np.float32)
+        for op in ("sum", "mean", "max"):
+            np.testing.assert_array_equal(oracle.segment_reduce(X, idx, S, op).absum, _brute_absum(X, idx, S))
+        # bf16 inputs: A from the bf16-valued inputs
+        bits = synth.f32_to_bf16_bits(X)
+        np.testing.assert_array_equal(oracle.segment_reduce(bits, idx, S, "sum").absum,
+                                      _brute_absum(synth.bf16_bits_to_f32(bits), idx, S))
+
+
+def test_absum_fused_and_weighted():
+    """Fused form: A = sum |x[src[e]]|; weighted: A = sum |w[e] * x[src[e]]|
+    (signed weights, so |w x| != w |x|)."""
+    rng = np.random.default_rng(33)
+    for trial in range(40):
+        E, S, V, F = int(rng.integers(0, 40)), int(rng.integers(1, 8)), int(rng.integers(1, 9)), int(rng.integers(1, 4))
+        dst = np.sort(rng.integers(0, S, size=E))
+        src = rng.integers(0, V, size=E)
+        x = (rng.random((V, F)) * 2 - 1).astype(np.float32)
+        w = (rng.random(E) * 2 - 1).astype(np.float32)
+        r = oracle.gather_segment_reduce(x, src, dst, S, "sum")
+        np.testing.assert_array_equal(r.absum, _brute_absum(x, dst, S, src=src))
+        rw = oracle.gather_segment_reduce(x, src, dst, S, "sum", weight=w)
+        np.testing.assert_array_equal(rw.absum, _brute_absum(x, dst, S, src=src, w=w))
+        assert np.all(rw.absum >= np.abs(rw.y64))  # triangle inequality
+
+
+def test_absum_bounds_sum_and_empty_rows_zero():
+    """|Y| <= A everywhere (triangle inequality), and empty segments have A = 0."""
+    L = synth.stress_lengths("gaps", 5000, 400, seed=6)
+    idx = synth.lengths_to_index(L)
+    X = synth.values_f32(10, 0, 5000, 4, "f32", "signed")
+    r = oracle.segment_reduce(X, idx, 400, "sum")
+    assert np.all(r.absum >= np.abs(r.y64))
+    assert np.all(r.absum[L == 0] == 0) and np.any(L == 0)
+    assert np.all(r.absum[L > 0] > 0)
