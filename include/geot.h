@@ -283,6 +283,59 @@ geot_status geot_validate_index(const void* idx, geot_itype itype, int64_t nnz, 
 geot_status geot_partition(const void* idx, geot_itype itype, int64_t nnz, int64_t num_segments,
                            int nparts, int64_t* seg_bounds, int64_t* edge_bounds, cudaStream_t stream);
 
+/* f4 / SURVEY §8(e) "Alternative partition (not default)": EXACT edge split
+ * with a one-step exchange of the straddling partials.  For p = 0..nparts:
+ *   t_p = floor(p * nnz / nparts)                       (edge_bounds: exact)
+ *   s_0 = 0;  s_nparts = num_segments;  s_p = (t_p == 0) ? 0 : idx[t_p - 1] + 1
+ *   boundary_keys[2p] = (t_p > 0) ? idx[t_p - 1] : -1;  boundary_keys[2p+1] = (t_p < nnz) ? idx[t_p] : -1
+ * Part p reduces edges [t_p, t_{p+1}) and owns rows [s_p, s_{p+1}).  Where
+ * idx[t_p - 1] == idx[t_p] the segment STRADDLES split p: it belongs to the
+ * lower part (the one holding edge t_p - 1), and every higher part it reaches
+ * contributes an fp32 partial (geot_segment_reduce_split) that the owner folds
+ * in rank order (geot_combine_partials) — DESIGN.md reading R21.  Balance is
+ * exact (|part| = floor or ceil of nnz/nparts) at the price of that exchange;
+ * geot_partition (H9) needs no exchange but may be unbalanced by a hub.
+ *   seg_bounds, edge_bounds  int64 [nparts + 1], device, write-only
+ *   boundary_keys            int64 [2 * (nparts + 1)], device, write-only
+ * Bit-exact.  nparts < 1, nnz < 0 or num_segments < 0 -> GEOT_ERR_INVALID_VALUE. */
+geot_status geot_partition_exact(const void* idx, geot_itype itype, int64_t nnz, int64_t num_segments, int nparts,
+                                 int64_t* seg_bounds, int64_t* edge_bounds, int64_t* boundary_keys,
+                                 cudaStream_t stream);
+
+/* Workspace of geot_segment_reduce_split (device bytes; zero-filled once, as
+ * for geot_workspace_size, which it includes). */
+size_t geot_split_workspace_size(int64_t nnz, int64_t num_segments, int64_t F, geot_reduce op, geot_dtype dtype,
+                                 geot_itype itype, const geot_config* cfg);
+
+/* One part of the exact split: geot_segment_reduce_ex over the part's edges
+ * (rows [seg_base, seg_base + num_segments), the head segment's row, which
+ * lies below seg_base when it straddles, is not written) PLUS the fp32
+ * partials of
+ *   slot 0: the head part, edges with key == idx[0]       (if head_open)
+ *   slot 1: the tail part, edges with key == idx[nnz - 1] (if tail_open)
+ * in partials[slot * F .. slot * F + F) (fp32, device) with their edge counts
+ * in counts[slot] (int64, device); a closed slot gets count 0 and the op's
+ * identity.  Each partial folds its rows in ascending order in chunks of 1024
+ * and the chunks in order (deterministic).  When tail_open the tail key's row
+ * holds only this part's edges until geot_combine_partials overwrites it.
+ * head_open / tail_open come from geot_partition_exact's boundary keys
+ * (idx[t_p - 1] == idx[t_p]); the part itself never reads past its edges. */
+geot_status geot_segment_reduce_split(const void* src, const void* idx, int64_t nnz, int64_t seg_base,
+                                      int64_t num_segments, int64_t F, geot_reduce op, geot_dtype dtype,
+                                      geot_itype itype, int head_open, int tail_open, void* out, float* partials,
+                                      int64_t* counts, void* workspace, size_t ws_bytes, const geot_config* cfg,
+                                      cudaStream_t stream);
+
+/* The owner's fold of a straddling segment: out_row[f] = finalize(fold over
+ * k < nslots of partials[h_slots[k] * F + f]) with count = sum of
+ * counts[h_slots[k]] (sum; mean = one fp32 division; max), stored in dtype.
+ *   partials [*, F] fp32 and counts [*] int64: every part's two slots after
+ *            the exchange (part q's head = slot 2q, tail = 2q + 1), device
+ *   h_slots  host array of nslots (1..64) slot ids, folded in that order
+ *   out_row  F elements (dtype), device.  Deterministic. */
+geot_status geot_combine_partials(const float* partials, const int64_t* counts, const int32_t* h_slots, int nslots,
+                                  int64_t F, geot_reduce op, geot_dtype dtype, void* out_row, cudaStream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

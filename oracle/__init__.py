@@ -54,6 +54,8 @@ def _load(path):
     L.oracle_gather_segment_reduce.restype = i32
     L.oracle_partition.argtypes = [vp, i32, i64, i64, i32, vp, vp]
     L.oracle_partition.restype = i32
+    L.oracle_partition_exact.argtypes = [vp, i32, i64, i64, i32, vp, vp, vp]
+    L.oracle_partition_exact.restype = i32
     L.oracle_segment_reduce_backward.argtypes = [vp, vp, i32, vp, i32, i64, i64, i64, i32, vp]
     L.oracle_segment_reduce_backward.restype = i32
     L.oracle_gather_segment_reduce_backward.argtypes = [vp, vp, i64, vp, vp, i32, vp, i64, i64, i64, i32, vp,
@@ -211,3 +213,15 @@ def partition(idx, S, nparts):
     if rc:
         raise ValueError("oracle_partition rejected its arguments")
     return sb, eb
+
+
+def partition_exact(idx, S, nparts):
+    """Exact edge split (R21): (seg_bounds, edge_bounds, boundary_keys [nparts+1, 2])."""
+    idx, it = _index(idx)
+    sb = np.zeros(nparts + 1, dtype=np.int64)
+    eb = np.zeros(nparts + 1, dtype=np.int64)
+    keys = np.zeros((nparts + 1, 2), dtype=np.int64)
+    rc = lib().oracle_partition_exact(_ptr(idx), it, idx.shape[0], S, nparts, _ptr(sb), _ptr(eb), _ptr(keys))
+    if rc:
+        raise ValueError("oracle_partition_exact rejected its arguments")
+    return sb, eb, keys

@@ -288,6 +288,36 @@ int oracle_partition(const void* idx, int itype, int64_t nnz, int64_t S, int npa
 }
 
 /* ---------------------------------------------------------------------------
+ * Exact edge split (SURVEY.md §8(e) "Alternative partition": exact
+ * floor(pE/P) edge splits, the straddling segment combined by an exchange;
+ * DESIGN.md reading R21): for p = 0..P,
+ *   t_p = floor(p*E/P)                                  (edge bounds)
+ *   s_0 = 0, s_P = S, s_p = (t_p == 0) ? 0 : idx[t_p - 1] + 1
+ *   keys[2p] = (t_p > 0) ? idx[t_p - 1] : -1,  keys[2p+1] = (t_p < E) ? idx[t_p] : -1
+ * The result of the split reduction itself is the plain segment reduction
+ * above (oracle_segment_reduce); only the bounds are defined here.
+ * ------------------------------------------------------------------------- */
+int oracle_partition_exact(const void* idx, int itype, int64_t nnz, int64_t S, int nparts,
+                           int64_t* seg_bounds, int64_t* edge_bounds, int64_t* keys) {
+    if (nparts < 1 || nnz < 0 || S < 0) return -1;
+    for (int p = 0; p <= nparts; ++p) {
+        const int64_t tp = (int64_t)(((__int128)p * nnz) / nparts);
+        const int64_t before = tp > 0 ? get_index(idx, itype, tp - 1) : -1;
+        const int64_t at = tp < nnz ? get_index(idx, itype, tp) : -1;
+        if (p == 0)
+            seg_bounds[p] = 0;
+        else if (p == nparts)
+            seg_bounds[p] = S;
+        else
+            seg_bounds[p] = tp == 0 ? 0 : before + 1;
+        edge_bounds[p] = tp;
+        keys[2 * p] = before;
+        keys[2 * p + 1] = at;
+    }
+    return 0;
+}
+
+/* ---------------------------------------------------------------------------
  * Gradients (the paper defers autograd):
  * the derivative of the definition above, as a vector-Jacobian product with
  * the output gradient dY (fp64, [S, F]):

@@ -29,7 +29,8 @@ _L = _lib.load()  # raises if libgeot.so is absent: no fallback
 __all__ = [
     "geot_segment_reduce", "geot_gather_segment_reduce", "geot_gather_weight_segment_reduce",
     "geot_segment_offsets", "geot_validate_index", "geot_partition", "geot_select_config",
-    "geot_workspace_size", "geot_launch_count", "segment_reduce", "index_segment_reduce",
+    "geot_workspace_size", "geot_launch_count", "geot_partition_exact", "geot_segment_reduce_split",
+    "geot_combine_partials", "segment_reduce", "index_segment_reduce",
     "index_weight_segment_reduce", "GeotConfig", "GeotError",
 ]
 
@@ -237,6 +238,61 @@ def geot_partition(idx, num_segments, nparts):
         _lib.check(_L.geot_partition(_ptr(idx), _it(idx), idx.numel(), num_segments, nparts, _ptr(sb), _ptr(eb),
                                      _stream(dev)), "geot_partition")
     return sb, eb
+
+
+def geot_partition_exact(idx, num_segments, nparts):
+    """Exact edge split (include/geot.h, R21): (seg_bounds, edge_bounds,
+    boundary_keys [nparts+1, 2] = {idx[t_p - 1], idx[t_p]} or -1), int64 device tensors."""
+    dev = _dev(idx)
+    sb = torch.empty(nparts + 1, dtype=torch.int64, device=dev)
+    eb = torch.empty(nparts + 1, dtype=torch.int64, device=dev)
+    keys = torch.empty((nparts + 1, 2), dtype=torch.int64, device=dev)
+    with torch.cuda.device(dev):
+        _lib.check(_L.geot_partition_exact(_ptr(idx), _it(idx), idx.numel(), num_segments, nparts, _ptr(sb), _ptr(eb),
+                                           _ptr(keys), _stream(dev)), "geot_partition_exact")
+    return sb, eb, keys
+
+
+def geot_segment_reduce_split(src, idx, seg_base, num_segments, op="sum", head_open=False, tail_open=False,
+                              out=None, cfg=None):
+    """One part of the exact split: (out, partials [2, F] fp32, counts [2] int64); see include/geot.h."""
+    dev = _dev(src, idx, out)
+    if src.dim() != 2 or idx.dim() != 1 or src.shape[0] != idx.shape[0]:
+        raise ValueError("src must be [nnz, F] and idx [nnz]")
+    E, F = src.shape
+    S = int(num_segments)
+    if out is None:
+        out = torch.empty((S, F), dtype=src.dtype, device=dev)
+    elif out.shape != (S, F) or out.dtype != src.dtype:
+        raise ValueError("out must be [num_segments, F] with src's dtype")
+    part = torch.empty((2, F), dtype=torch.float32, device=dev)
+    cnt = torch.empty(2, dtype=torch.int64, device=dev)
+    ws_n = _L.geot_split_workspace_size(E, S, F, _op(op), _dt(src), _it(idx), _cfgp(cfg))
+    ws, ws_bytes = _workspace(dev, ws_n)
+    with torch.cuda.device(dev):
+        st = _L.geot_segment_reduce_split(_ptr(src), _ptr(idx), E, seg_base, S, F, _op(op), _dt(src), _it(idx),
+                                          int(bool(head_open)), int(bool(tail_open)), _ptr(out), _ptr(part),
+                                          _ptr(cnt), _ptr(ws), ws_bytes, _cfgp(cfg), _stream(dev))
+    _lib.check(st, "geot_segment_reduce_split")
+    return out, part, cnt
+
+
+def geot_combine_partials(partials, counts, slots, out_row, op="sum"):
+    """out_row = finalize(fold of partials[slots] in order) (include/geot.h)."""
+    dev = _dev(partials, counts, out_row)
+    if partials.dtype != torch.float32 or counts.dtype != torch.int64:
+        raise TypeError("partials must be float32 and counts int64")
+    F = partials.shape[-1]
+    if out_row.numel() != F:
+        raise ValueError("out_row must hold F elements")
+    n = partials.numel() // F
+    if any(not 0 <= int(s_) < n for s_ in slots) or not 1 <= len(slots) <= 64:
+        raise ValueError("1..64 slot ids within the partials")
+    arr = (ctypes.c_int32 * len(slots))(*[int(s_) for s_ in slots])
+    with torch.cuda.device(dev):
+        _lib.check(_L.geot_combine_partials(_ptr(partials), _ptr(counts), arr, len(slots), F, _op(op), _dt(out_row),
+                                            _ptr(out_row), _stream(dev)), "geot_combine_partials")
+    return out_row
 
 
 def geot_segment_reduce_backward(grad_out, idx, op="sum", offsets=None, src=None, out=None, grad_src=None):

@@ -74,6 +74,11 @@ SIGNATURES = {
                                              _vp, _vp], _i32),
     "geot_validate_index": ([_vp, _i32, _i64, _i64, _vp, _i64, _vp, _vp], _i32),
     "geot_partition": ([_vp, _i32, _i64, _i64, _i32, _vp, _vp, _vp], _i32),
+    "geot_partition_exact": ([_vp, _i32, _i64, _i64, _i32, _vp, _vp, _vp, _vp], _i32),
+    "geot_split_workspace_size": ([_i64, _i64, _i64, _i32, _i32, _i32, _cfgp], _sz),
+    "geot_segment_reduce_split": ([_vp, _vp, _i64, _i64, _i64, _i64, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp,
+                                   _vp, _sz, _cfgp, _vp], _i32),
+    "geot_combine_partials": ([_vp, _vp, ctypes.POINTER(ctypes.c_int32), _i32, _i64, _i32, _i32, _vp, _vp], _i32),
 }
 
 _lib = None

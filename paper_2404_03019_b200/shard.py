@@ -83,3 +83,74 @@ def open_peer_replicas(local_full, group=None):
     me = dist.get_rank(group)
     return [local_full if r == me else fn(*args) for r, (fn, args) in enumerate(objs)]
 
+
+
+# ---------------------------------------------------------------------------
+# f4 "Alternative partition": the exact edge split with a one-step exchange
+# (include/geot.h geot_partition_exact / geot_segment_reduce_split /
+# geot_combine_partials; reading R21).  Pure host logic here: the
+# plan is derived once per graph from the partition's bounds and boundary keys.
+def split_plan(seg_bounds: Sequence[int], edge_bounds: Sequence[int], boundary_keys):
+    """Per part p: its edges/rows, whether its head / tail piece straddles a
+    split, and — for the part that holds a straddling segment's FIRST edge (the
+    owner) — the slot chain to fold (own tail = slot 2p + 1, then the head
+    piece 2q of every later part q the segment reaches, in rank order) and the
+    local output row of that segment.  boundary_keys[p] = (idx[t_p - 1],
+    idx[t_p]) with -1 outside the edge range."""
+    P = len(edge_bounds) - 1
+    keys = [(int(boundary_keys[p][0]), int(boundary_keys[p][1])) for p in range(P + 1)]
+    eb = [int(e) for e in edge_bounds]
+    sb = [int(s) for s in seg_bounds]
+    # split p cuts a segment: the edges on both sides of t_p share their key
+    cut = [0 < p < P and keys[p][0] >= 0 and keys[p][0] == keys[p][1] for p in range(P + 1)]
+    plans = []
+    for p in range(P):
+        n = eb[p + 1] - eb[p]
+        head = cut[p] and n > 0
+        tail = cut[p + 1] and n > 0
+        middle = n > 0 and keys[p][1] == keys[p + 1][0]  # first key == last key: one segment
+        plan = {"e0": eb[p], "e1": eb[p + 1], "s0": sb[p], "s1": sb[p + 1], "head_open": head,
+                "tail_open": tail, "chain": None, "row": None}
+        if tail and not (head and middle):  # the straddling tail segment begins here: owner
+            chain, q = [2 * p + 1], p + 1
+            while q < P:
+                nq = eb[q + 1] - eb[q]
+                if nq > 0:
+                    chain.append(2 * q)
+                if cut[q + 1] and (nq == 0 or keys[q][1] == keys[q + 1][0]):
+                    q += 1  # the segment covers part q entirely and continues
+                    continue
+                break
+            plan["chain"] = chain
+            plan["row"] = keys[p + 1][0] - sb[p]
+        plans.append(plan)
+    return plans
+
+
+def exchange_partials(part, cnt, group=None):
+    """All-gather every part's [2, F] fp32 partials and [2] counts (the one
+    exchange step; NCCL on GPUs, CPU tensors under gloo).  Returns
+    ([P * 2, F], [P * 2]) on part's device."""
+    import torch
+    import torch.distributed as dist
+    P = dist.get_world_size(group)
+    on_dev = dist.get_backend(group) == "nccl"
+    p_, c_ = (part, cnt) if on_dev else (part.cpu(), cnt.cpu())
+    parts = [torch.empty_like(p_) for _ in range(P)]
+    cnts = [torch.empty_like(c_) for _ in range(P)]
+    dist.all_gather(parts, p_.contiguous(), group=group)
+    dist.all_gather(cnts, c_.contiguous(), group=group)
+    return torch.cat(parts, 0).to(part.device), torch.cat(cnts, 0).to(cnt.device)
+
+
+def exact_split_reduce(src, idx, plan, op="sum", out=None, group=None, cfg=None):
+    """One rank of the exact-split reduction: reduce the part (rows
+    [s0, s1)), exchange the straddling partials, fold the owned straddling row.
+    src / idx are this part's edges [e0, e1) of the global arrays."""
+    import paper_2404_03019_b200 as geot
+    out, part, cnt = geot.geot_segment_reduce_split(src, idx, plan["s0"], plan["s1"] - plan["s0"], op,
+                                                    plan["head_open"], plan["tail_open"], out=out, cfg=cfg)
+    all_p, all_c = exchange_partials(part, cnt, group)
+    if plan["chain"]:
+        geot.geot_combine_partials(all_p, all_c, plan["chain"], out[plan["row"]], op)
+    return out

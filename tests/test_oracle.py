@@ -481,3 +481,41 @@ def test_absum_bounds_sum_and_empty_rows_zero():
     assert np.all(r.absum >= np.abs(r.y64))
     assert np.all(r.absum[L == 0] == 0) and np.any(L == 0)
     assert np.all(r.absum[L > 0] > 0)
+
+
+# ------------------------------------------------------ exact split (R21)
+@pytest.mark.parametrize("name", ["W1", "W2"])
+def test_partition_exact_worked(golden, name):
+    """Hand constants (tests/golden/worked_examples.json) of the exact edge
+    split, SURVEY.md §8(e) 'Alternative partition', R21."""
+    c = golden["worked_examples"][name]
+    for P, b in c["partition_exact"].items():
+        sb, eb, keys = oracle.partition_exact(np.array(c["dst"]), c["S"], int(P))
+        np.testing.assert_array_equal(sb, b["seg"])
+        np.testing.assert_array_equal(eb, b["edge"])
+        np.testing.assert_array_equal(keys, b["keys"])
+
+
+def test_partition_exact_invariants():
+    """Edge bounds are exactly floor(pE/P) (balance within one edge); row
+    bounds are monotone, cover [0, S), and every segment's row lies in the part
+    holding its first edge; the keys are the edges on both sides of each split."""
+    rng = np.random.default_rng(15)
+    for _ in range(800):
+        S = int(rng.integers(1, 25))
+        E = int(rng.integers(0, 70))
+        idx = np.sort(rng.integers(0, S, size=E))
+        P = int(rng.integers(1, 10))
+        sb, eb, keys = oracle.partition_exact(idx, S, P)
+        np.testing.assert_array_equal(eb, [(p * E) // P for p in range(P + 1)])
+        assert sb[0] == 0 and sb[-1] == S and np.all(np.diff(sb) >= 0)
+        for p in range(P + 1):
+            assert keys[p, 0] == (idx[eb[p] - 1] if eb[p] > 0 else -1)
+            assert keys[p, 1] == (idx[eb[p]] if eb[p] < E else -1)
+        first = np.searchsorted(idx, np.arange(S))  # first edge of every segment (E if empty)
+        for s in range(S):
+            if first[s] < E and idx[first[s]] == s:
+                owner = int(np.searchsorted(eb, first[s], side="right") - 1)
+                while eb[owner] == eb[owner + 1]:  # skip empty parts
+                    owner += 1
+                assert sb[owner] <= s < sb[owner + 1], (s, owner, sb, eb)

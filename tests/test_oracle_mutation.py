@@ -34,6 +34,8 @@ MUTANTS = [
     ("bf16_truncates", "u += 0x7FFFu + lsb;", "u += 0;"),
     ("bf16_round_half_up", "u += 0x7FFFu + lsb;", "u += 0x8000u;"),
     ("partition_no_plus_one", "get_index(idx, itype, tp - 1) + 1", "get_index(idx, itype, tp - 1)"),
+    ("exact_split_no_plus_one", "seg_bounds[p] = tp == 0 ? 0 : before + 1;", "seg_bounds[p] = tp == 0 ? 0 : before;"),
+    ("exact_split_keys_swapped", "keys[2 * p] = before;", "keys[2 * p] = at;"),
     ("validate_unsorted_missed", "get_index(idx, itype, e - 1) > s", "get_index(idx, itype, e - 1) > s + 1"),
 ]
 
@@ -56,7 +58,8 @@ def _pins(golden):
              T.test_partition_invariants, T.test_validate_bits, T.test_empty_inputs,
              T.test_absum_single_segment_is_numpy_abs_column_sum, T.test_absum_equals_sum_for_nonnegative_inputs,
              T.test_absum_signed_brute_force, T.test_absum_fused_and_weighted,
-             T.test_absum_bounds_sum_and_empty_rows_zero]
+             T.test_absum_bounds_sum_and_empty_rows_zero, T.test_partition_exact_invariants]
+    pins += [lambda name=name: T.test_partition_exact_worked(golden, name) for name in ("W1", "W2")]
     return pins
 
 
