@@ -163,6 +163,17 @@ size_t geot_workspace_size(int64_t nnz, int64_t num_segments, int64_t F, geot_re
  * (cudaMemsetAsync).  Needed once per workspace allocation. */
 geot_status geot_workspace_init(void* workspace, size_t ws_bytes, cudaStream_t stream);
 
+/* Health of a workspace (SYNCHRONOUS: reads its control words after
+ * synchronising `stream`; a diagnostic, not for the hot path).  *h_status
+ * (host) = 0 healthy; bit 1 = poisoned: some call drew an out-of-range ticket
+ * because the workspace was not zero-filled before first use or was used by
+ * two calls at once — such a call retires without writing its output (no trap,
+ * no hang) and the flag stays set until geot_workspace_init; bit 2 = the
+ * control words are not at rest (a call is in flight on another stream, or a
+ * poisoned call left them so).  Recovery: geot_workspace_init, then repeat the
+ * call.  NULL / tiny workspaces report 0. */
+geot_status geot_workspace_status(const void* workspace, size_t ws_bytes, cudaStream_t stream, int32_t* h_status);
+
 /* H4-H7: sorted-index segment reduction (Fig. 2; Alg. 1's result).
  *   src        [nnz, F] values (dtype), device
  *   idx        [nnz] non-decreasing segment ids (itype), device
@@ -335,6 +346,17 @@ geot_status geot_segment_reduce_split(const void* src, const void* idx, int64_t 
  *   out_row  F elements (dtype), device.  Deterministic. */
 geot_status geot_combine_partials(const float* partials, const int64_t* counts, const int32_t* h_slots, int nslots,
                                   int64_t F, geot_reduce op, geot_dtype dtype, void* out_row, cudaStream_t stream);
+
+/* Self-test hook (tests only; nothing on the hot path calls it): runs the
+ * narrow kernel's warp segmented scan (the warp pass of Alg. 1, P:199-205;
+ * narrow.cuh warp_segscan) on nwarps x 32 (key, value) items, one item per
+ * lane, a segment starting in lane l when l == 0 or keys[l] != keys[l-1].
+ * Per lane: out_vals = fold (sum for GEOT_SUM / GEOT_MEAN, max for GEOT_MAX)
+ * of the values from its segment's first lane through itself, out_flags = 1,
+ * out_pos = that first lane's index (propagated for GEOT_MEAN only, else 0
+ * except at starts).  All pointers device, [nwarps * 32]. */
+geot_status geot_selftest_warp_segscan(const int32_t* keys, const float* vals, int64_t nwarps, geot_reduce op,
+                                       float* out_vals, int32_t* out_flags, int64_t* out_pos, cudaStream_t stream);
 
 #ifdef __cplusplus
 }

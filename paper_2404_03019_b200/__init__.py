@@ -30,7 +30,7 @@ __all__ = [
     "geot_segment_reduce", "geot_gather_segment_reduce", "geot_gather_weight_segment_reduce",
     "geot_segment_offsets", "geot_validate_index", "geot_partition", "geot_select_config",
     "geot_workspace_size", "geot_launch_count", "geot_partition_exact", "geot_segment_reduce_split",
-    "geot_combine_partials", "segment_reduce", "index_segment_reduce",
+    "geot_combine_partials", "geot_workspace_check", "segment_reduce", "index_segment_reduce",
     "index_weight_segment_reduce", "GeotConfig", "GeotError",
 ]
 
@@ -108,6 +108,45 @@ def _workspace(dev, nbytes):
     return buf, buf.numel()
 
 
+def _ws_status(dev, buf):
+    h = ctypes.c_int32(0)
+    with torch.cuda.device(dev):
+        _lib.check(_L.geot_workspace_status(_ptr(buf), buf.numel(), _stream(dev), ctypes.byref(h)),
+                   "geot_workspace_status")
+    return int(h.value)
+
+
+def geot_workspace_check(repair=True):
+    """Synchronising health check of every cached workspace (include/geot.h
+    geot_workspace_status): {(device, stream): status}; a poisoned one (bit 1)
+    is re-initialised when repair is set."""
+    res = {}
+    with _ws_lock:
+        items = list(_ws_cache.items())
+    for (dev, sid), buf in items:
+        st = _ws_status(dev, buf)
+        if st & 1 and repair:
+            with torch.cuda.device(dev):
+                _lib.check(_L.geot_workspace_init(_ptr(buf), buf.numel(), _stream(dev)), "geot_workspace_init")
+        res[(dev, sid)] = st
+    return res
+
+
+def _checked(dev, run):
+    """Run a reduction, then verify its workspace; on poison re-initialise it and
+    run once more (the output of a poisoned call is not written)."""
+    run()
+    key = (dev, torch.cuda.current_stream(dev).cuda_stream)
+    buf = _ws_cache.get(key)
+    if buf is None or not _ws_status(dev, buf) & 1:
+        return
+    with torch.cuda.device(dev):
+        _lib.check(_L.geot_workspace_init(_ptr(buf), buf.numel(), _stream(dev)), "geot_workspace_init")
+    run()
+    if _ws_status(dev, buf) & 1:
+        raise GeotError(1, "workspace poisoned again after re-initialisation (concurrent use of one stream's workspace?)")
+
+
 def geot_launch_count() -> int:
     return int(_L.geot_launch_count())
 
@@ -158,8 +197,10 @@ def _num_segments(idx, num_segments):
     return int(idx[-1].item()) + 1 if idx.numel() else 0  # device->host read (documented)
 
 
-def geot_segment_reduce(src, idx, num_segments=None, op="sum", out=None, seg_base=0, cfg=None):
-    """out[r,:] = op over {src[e,:] : idx[e] == seg_base + r}."""
+def geot_segment_reduce(src, idx, num_segments=None, op="sum", out=None, seg_base=0, cfg=None, checked=False):
+    """out[r,:] = op over {src[e,:] : idx[e] == seg_base + r}.
+    checked=True synchronises after the call and repairs a poisoned workspace
+    (geot_workspace_check), re-running the call once."""
     dev = _dev(src, idx, out)
     if src.dim() != 2 or idx.dim() != 1 or src.shape[0] != idx.shape[0]:
         raise ValueError("src must be [nnz, F] and idx [nnz]")
@@ -170,11 +211,18 @@ def geot_segment_reduce(src, idx, num_segments=None, op="sum", out=None, seg_bas
     elif out.shape != (S, F) or out.dtype != src.dtype:
         raise ValueError("out must be [num_segments, F] with src's dtype")
     ws_n = _L.geot_workspace_size(E, S, F, _op(op), _dt(src), _it(idx), 0, _cfgp(cfg))
-    ws, ws_bytes = _workspace(dev, ws_n)
-    with torch.cuda.device(dev):
-        st = _L.geot_segment_reduce_ex(_ptr(src), _ptr(idx), E, seg_base, S, F, _op(op), _dt(src), _it(idx),
-                                       _ptr(out), _ptr(ws), ws_bytes, _cfgp(cfg), _stream(dev))
-    _lib.check(st, "geot_segment_reduce")
+
+    def run():
+        ws, ws_bytes = _workspace(dev, ws_n)
+        with torch.cuda.device(dev):
+            st = _L.geot_segment_reduce_ex(_ptr(src), _ptr(idx), E, seg_base, S, F, _op(op), _dt(src), _it(idx),
+                                           _ptr(out), _ptr(ws), ws_bytes, _cfgp(cfg), _stream(dev))
+        _lib.check(st, "geot_segment_reduce")
+
+    if checked:
+        _checked(dev, run)
+    else:
+        run()
     return out
 
 

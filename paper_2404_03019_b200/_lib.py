@@ -54,6 +54,7 @@ SIGNATURES = {
     "geot_select_config": ([_i64, _i64, _i64, _i32, _i32, _i32, _i32, _cfgp], _i32),
     "geot_workspace_size": ([_i64, _i64, _i64, _i32, _i32, _i32, _i32, _cfgp], _sz),
     "geot_workspace_init": ([_vp, _sz, _vp], _i32),
+    "geot_workspace_status": ([_vp, _sz, _vp, ctypes.POINTER(ctypes.c_int32)], _i32),
     "geot_select_tree": ([ctypes.c_double] * 5 + [ctypes.POINTER(ctypes.c_int32)], None),
     "geot_selector_provenance": ([], ctypes.c_char_p),
     "geot_segment_reduce": ([_vp, _vp, _i64, _i64, _i64, _i32, _i32, _i32, _vp, _vp, _sz, _vp], _i32),
@@ -78,6 +79,7 @@ SIGNATURES = {
     "geot_split_workspace_size": ([_i64, _i64, _i64, _i32, _i32, _i32, _cfgp], _sz),
     "geot_segment_reduce_split": ([_vp, _vp, _i64, _i64, _i64, _i64, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp,
                                    _vp, _sz, _cfgp, _vp], _i32),
+    "geot_selftest_warp_segscan": ([_vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp], _i32),
     "geot_combine_partials": ([_vp, _vp, ctypes.POINTER(ctypes.c_int32), _i32, _i64, _i32, _i32, _vp, _vp], _i32),
 }
 

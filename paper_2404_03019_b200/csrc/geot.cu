@@ -499,6 +499,18 @@ geot_status geot_workspace_init(void* workspace, size_t ws_bytes, cudaStream_t s
     return from_cuda(cudaMemsetAsync(workspace, 0, ws_bytes, stream));
 }
 
+geot_status geot_workspace_status(const void* workspace, size_t ws_bytes, cudaStream_t stream, int32_t* h_status) {
+    if (!h_status) return GEOT_ERR_INVALID_VALUE;
+    *h_status = 0;
+    if (!workspace || ws_bytes < sizeof(StreamCtrl)) return GEOT_OK;  // no control words
+    StreamCtrl c;
+    cudaError_t e = cudaMemcpyAsync(&c, workspace, sizeof(c), cudaMemcpyDeviceToHost, stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+    if (e != cudaSuccess) return from_cuda(e);
+    *h_status = (c.poison ? 1 : 0) | ((c.ticket != 0 || c.done != 0) ? 2 : 0);
+    return GEOT_OK;
+}
+
 geot_status geot_segment_reduce(const void* src, const void* idx, int64_t nnz, int64_t num_segments, int64_t F,
                                 geot_reduce op, geot_dtype dtype, geot_itype itype, void* out, void* workspace,
                                 size_t ws_bytes, cudaStream_t stream) {

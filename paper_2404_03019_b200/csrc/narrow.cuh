@@ -174,6 +174,34 @@ __device__ __forceinline__ float nident() {
     return identity<OP == OP_MAX>();
 }
 
+// The warp pass of Alg. 1 (the __shfl doubling loop): a segmented
+// inclusive scan over the 32 lanes.  In: sv = the lane's value, sf = "a segment
+// starts in this lane" (reset flag), spos = that start's position (mean only).
+// Out: sv = fold of the values from the nearest lane <= this one whose flag is
+// set (or from lane 0) through this lane; sf = whether such a lane exists;
+// spos = its position.  log2(32) = 5 steps; lane l takes lane l-d's partial
+// only while its own chain has not reached a segment start.  (Checked on every
+// non-decreasing 8-key sequence and on random 16/32-lane sequences by
+// geot_selftest_warp_segscan.)
+template <int F, int OP>
+__device__ __forceinline__ void warp_segscan(float (&sv)[F], bool& sf, long long& spos, int lane) {
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        float ov[F];
+#pragma unroll
+        for (int f = 0; f < F; ++f) ov[f] = __shfl_up_sync(0xffffffffu, sv[f], d);
+        const bool of = __shfl_up_sync(0xffffffffu, (int)sf, d) != 0;
+        long long op_ = 0;
+        if constexpr (OP == OP_MEAN) op_ = __shfl_up_sync(0xffffffffu, spos, d);
+        if (lane >= d && !sf) {
+#pragma unroll
+            for (int f = 0; f < F; ++f) sv[f] = nfold<OP>(ov[f], sv[f]);
+            sf = of;
+            if constexpr (OP == OP_MEAN) spos = op_;
+        }
+    }
+}
+
 template <typename T, int F, int ITEMS, int OP, bool I64>
 __global__ void __launch_bounds__(kNarrowWarps * 32, 2)
     narrow_kernel(const __grid_constant__ CUtensorMap tmv, const __grid_constant__ CUtensorMap tmk,
@@ -204,12 +232,10 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, 2)
 
     __shared__ unsigned s_ticket;
     __shared__ unsigned long long s_epoch;
-    if (threadIdx.x == 0) {
-        s_ticket = atomicAdd(&p.ctrl->ticket, 1u);
-        s_epoch = ld_acquire_u64(&p.ctrl->epoch);
-        if (s_ticket >= gridDim.x) __trap();  // workspace not zero-filled before first use
+    if (!draw_ticket(p.ctrl, &s_ticket, &s_epoch)) {  // poisoned workspace: retire (stream.cuh)
+        retire_cta(p.ctrl);
+        return;
     }
-    __syncthreads();
     const unsigned long long pub = s_epoch + 1;
     const long long a = (long long)s_ticket * kNarrowWarps + warp;
     auto agent_lo = [&](long long x) -> long long {
@@ -396,44 +422,36 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, 2)
         }
 
         // gaps (empty segments) or unsorted keys: a lane whose key span differs
-        // from its number of heads.  Rare per lane, but some lane of most chunks
-        // has one: the warp takes those lanes one at a time, lane i examining item
-        // i of the gap lane (keys from the ring) and zero-filling its gap
+        // from its number of heads.  Such a lane finds its gap items from the
+        // keys in its registers (bit i: k[i] - k[i-1] > 1, k[-1] = kp) and
+        // zero-fills each gap, reading the two keys of a gap back from its ring
+        // slot (a dynamic item index; no local memory).  Lanes without gaps idle.
         {
             const bool gap = nv > 0 && (long long)klast - (long long)kp != (long long)__popc(hm);
-            unsigned gl = __ballot_sync(0xffffffffu, gap);
-            while (gl) {
-                const int g = __ffs(gl) - 1;
-                gl &= gl - 1;
-                const KT gkp = __shfl_sync(0xffffffffu, kp, g);
-                const int gnv = __shfl_sync(0xffffffffu, nv, g);
-                const bool gdirect = __shfl_sync(0xffffffffu, (int)direct, g) != 0;
-                const long long gr0 = c0 + (long long)g * ITEMS;
-                long long kc = 0, kq = 0;  // key of item `lane` of lane g and of the item before it
-                if (lane < gnv) {
-                    if (!gdirect) {
-                        const uint32_t kb = ring + b * STAGE + AREA_V;
-                        if constexpr (I64) {
-                            unsigned long long t0, t1 = 0;
-                            asm volatile("ld.shared.u64 %0, [%1];" : "=l"(t0) : "r"(kb + swz<LBK>((uint32_t)(g * LBK + lane * 8))));
-                            if (lane > 0)
-                                asm volatile("ld.shared.u64 %0, [%1];" : "=l"(t1) : "r"(kb + swz<LBK>((uint32_t)(g * LBK + (lane - 1) * 8))));
-                            kc = (long long)t0;
-                            kq = (long long)t1;
-                        } else {
-                            int t0, t1 = 0;
-                            asm volatile("ld.shared.s32 %0, [%1];" : "=r"(t0) : "r"(kb + swz<LBK>((uint32_t)(g * LBK + lane * 4))));
-                            if (lane > 0)
-                                asm volatile("ld.shared.s32 %0, [%1];" : "=r"(t1) : "r"(kb + swz<LBK>((uint32_t)(g * LBK + (lane - 1) * 4))));
-                            kc = t0;
-                            kq = t1;
-                        }
+            if (__any_sync(0xffffffffu, gap) && gap) {
+                unsigned gm = 0;
+#pragma unroll
+                for (int i = 0; i < ITEMS; ++i) {
+                    const long long kq = i == 0 ? (long long)kp : (long long)k[i - 1];
+                    gm |= (unsigned)(i < nv && (long long)k[i] - kq > 1) << i;
+                }
+                const uint32_t kb = ring + b * STAGE + AREA_V;
+                auto key_item = [&](int i) -> long long {
+                    if (direct) return key_at(r0 + i);
+                    if constexpr (I64) {
+                        unsigned long long t;
+                        asm volatile("ld.shared.u64 %0, [%1];" : "=l"(t) : "r"(kb + swz<LBK>((uint32_t)(lane * LBK + i * 8))));
+                        return (long long)t;
                     } else {
-                        kc = key_at(gr0 + lane);
-                        kq = lane > 0 ? key_at(gr0 + lane - 1) : 0;
+                        int t;
+                        asm volatile("ld.shared.s32 %0, [%1];" : "=r"(t) : "r"(kb + swz<LBK>((uint32_t)(lane * LBK + i * 4))));
+                        return t;
                     }
-                    if (lane == 0) kq = (long long)gkp;
-                    if (kc - kq > 1) gap_fill(kq, kc);
+                };
+                while (gm) {
+                    const int i = __ffs(gm) - 1;
+                    gm &= gm - 1;
+                    gap_fill(i == 0 ? (long long)kp : key_item(i - 1), key_item(i));
                 }
             }
         }
@@ -444,21 +462,7 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, 2)
         for (int f = 0; f < F; ++f) sv[f] = acc[ITEMS - 1][f];
         bool sf = hm != 0;  // a segment starts in this lane (reset flag)
         long long spos = hm ? (r0 - e_lo) + (31 - __clz(hm)) : 0;  // start row of the lane's tail segment
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            float ov[F];
-#pragma unroll
-            for (int f = 0; f < F; ++f) ov[f] = __shfl_up_sync(0xffffffffu, sv[f], d);
-            const bool of = __shfl_up_sync(0xffffffffu, (int)sf, d) != 0;
-            long long op_ = 0;
-            if constexpr (OP == OP_MEAN) op_ = __shfl_up_sync(0xffffffffu, spos, d);
-            if (lane >= d && !sf) {
-#pragma unroll
-                for (int f = 0; f < F; ++f) sv[f] = nfold<OP>(ov[f], sv[f]);
-                sf = of;
-                if constexpr (OP == OP_MEAN) spos = op_;
-            }
-        }
+        warp_segscan<F, OP>(sv, sf, spos, lane);
         const bool reach = !sf;  // this lane's chain reaches back to the open segment
         if (reach) {
 #pragma unroll
@@ -573,33 +577,28 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, 2)
     __syncwarp();
     if (active && head_open && !(flags & TM_MIDDLE) && lane == 0) {
         long long u = a - 1;
+        bool ok = true;
         for (; u >= 0; --u) {
-            while (ld_acquire_u64(&p.flag[u]) != pub) {
+            if (!wait_flag_or_poison(&p.flag[u], pub, p.ctrl)) {
+                ok = false;
+                break;
             }
             if (!(ld_volatile_i32(&p.meta[u].flags) & TM_MIDDLE)) break;
         }
         if (u < 0) u = 0;
-        float tot[F];
+        if (ok) {
+            float tot[F];
 #pragma unroll
-        for (int f = 0; f < F; ++f) tot[f] = ld_cg_f32(p.carry_t + u * F + f);
-        for (long long m = u + 1; m < a; ++m)
+            for (int f = 0; f < F; ++f) tot[f] = ld_cg_f32(p.carry_t + u * F + f);
+            for (long long m = u + 1; m < a; ++m)
 #pragma unroll
-            for (int f = 0; f < F; ++f) tot[f] = nfold<OP>(tot[f], ld_cg_f32(p.carry_h + m * F + f));
+                for (int f = 0; f < F; ++f) tot[f] = nfold<OP>(tot[f], ld_cg_f32(p.carry_h + m * F + f));
 #pragma unroll
-        for (int f = 0; f < F; ++f) tot[f] = nfold<OP>(tot[f], hacc[f]);
-        store_at(true, (KT)first_key, tot, (int)(head_end - ld_volatile_i64(&p.meta[u].tail_start)));
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        const unsigned done = atomicAdd(&p.ctrl->done, 1u);
-        if (done == gridDim.x - 1) {
-            p.ctrl->done = 0;
-            p.ctrl->ticket = 0;
-            __threadfence();
-            atomicAdd(&p.ctrl->epoch, 1ull);
+            for (int f = 0; f < F; ++f) tot[f] = nfold<OP>(tot[f], hacc[f]);
+            store_at(true, (KT)first_key, tot, (int)(head_end - ld_volatile_i64(&p.meta[u].tail_start)));
         }
     }
+    retire_cta(p.ctrl);
 }
 
 }  // namespace geot

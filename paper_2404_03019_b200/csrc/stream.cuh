@@ -48,7 +48,53 @@ struct StreamCtrl {
     unsigned ticket;
     unsigned done;
     unsigned long long epoch;
+    unsigned poison;  // sticky: set when a CTA drew a ticket >= gridDim.x (a workspace
+                      // not zero-filled before first use, or used by two calls at
+                      // once); cleared only by geot_workspace_init
+    unsigned pad;
 };
+
+// CTA start: draw the ticket.  A ticket outside [0, gridDim.x) means the control
+// words were not in their rest state: flag the workspace (geot_workspace_status
+// reports it) and let the CTA retire without touching the output.  Agents that
+// wait on carries poll the flag, so nothing spins on agents that never run.
+__device__ __forceinline__ bool draw_ticket(StreamCtrl* ctrl, unsigned* s_ticket, unsigned long long* s_epoch) {
+    if (threadIdx.x == 0) {
+        *s_ticket = atomicAdd(&ctrl->ticket, 1u);
+        *s_epoch = ld_acquire_u64(&ctrl->epoch);
+        if (*s_ticket >= gridDim.x) atomicOr(&ctrl->poison, 1u);
+    }
+    __syncthreads();
+    return *s_ticket < gridDim.x;
+}
+
+// wait_flag_acquire that gives up (false) once the workspace is flagged poisoned
+__device__ __forceinline__ bool wait_flag_or_poison(const unsigned long long* p, unsigned long long v,
+                                                    const StreamCtrl* ctrl) {
+    unsigned long long x;
+    for (unsigned n = 0;; ++n) {
+        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(x) : "l"(p) : "memory");
+        if (x == v) break;
+        if ((n & 255u) == 255u && *reinterpret_cast<const volatile unsigned*>(&ctrl->poison)) return false;
+    }
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    return true;
+}
+
+// CTA end: the last CTA out re-arms ticket / done and advances the epoch.
+__device__ __forceinline__ void retire_cta(StreamCtrl* ctrl) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned done = atomicAdd(&ctrl->done, 1u);
+        if (done == gridDim.x - 1) {
+            ctrl->done = 0;
+            ctrl->ticket = 0;
+            __threadfence();
+            atomicAdd(&ctrl->epoch, 1ull);
+        }
+    }
+}
 
 struct StreamParams {
     const void* X;
@@ -145,12 +191,10 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
     // ever waits on agents of CTAs that started before it (forward progress).
     __shared__ unsigned s_ticket;
     __shared__ unsigned long long s_epoch;
-    if (threadIdx.x == 0) {
-        s_ticket = atomicAdd(&p.ctrl->ticket, 1u);
-        s_epoch = ld_acquire_u64(&p.ctrl->epoch);
-        if (s_ticket >= gridDim.x) __trap();  // workspace not zero-filled before first use
+    if (!draw_ticket(p.ctrl, &s_ticket, &s_epoch)) {
+        retire_cta(p.ctrl);
+        return;
     }
-    __syncthreads();
     const unsigned long long pub = s_epoch + 1;  // "published in this call" flag value
 
     // agent ranges (one 64-bit division per agent, once)
@@ -420,8 +464,11 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
     // SUB rows at a time (code size: the segment-end path is inlined once per
     // row of a sub-chunk); `heads` bit r = row r starts a segment; the key of
     // row r is held by lane (koff + r) of the group
+    // wst[r]: the weight of row r (MODE 2), read from the ring by every lane of
+    // the group (broadcast) before the stage's buffer is refilled — a shuffle
+    // with a group mask would cost a WARPSYNC loop per row
     auto process = [&](const Raw (&rows)[SUB][VPL], unsigned heads, long long kmine, int koff, int cnt,
-                       long long r_base, float wmine) {
+                       long long r_base, const float (&wst)[SUB]) {
 #pragma unroll
         for (int r = 0; r < SUB; ++r) {
             // (G >= 4: no early exit — the warp-wide votes below need every lane)
@@ -494,7 +541,7 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
                 if (!valid) continue;  // (no collective below this point)
             }
             float wr = 1.0f;
-            if constexpr (MODE == 2) wr = __shfl_sync(gmask, wmine, koff + r, LPR);
+            if constexpr (MODE == 2) wr = wst[r];
             if constexpr (PKMAX) {
 #pragma unroll
                 for (int j = 0; j < VPL; ++j) {
@@ -550,11 +597,11 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
             cnt = cnt < 0 ? 0 : (cnt > RS ? RS : cnt);
             const long long kmine = (li < cnt) ? gkey[li] : KEY_AFTER;
             const long long kprev = (li == 0) ? cur : ((li <= cnt) ? gkey[li - 1] : KEY_AFTER);
-            float wmine = 1.0f;
-            if constexpr (MODE == 2) wmine = (li < cnt) ? wring[(b * G + gi) * RS + li] : 0.0f;
+            const float* wslots = MODE == 2 ? wring + (b * G + gi) * RS : nullptr;
             // is_seg of the whole stage (Alg. 1): row r starts a segment iff its
-            // key differs from row r-1's (row -1: `cur`)
-            const unsigned heads = __ballot_sync(gmask, li < cnt && kmine != kprev) >> (gi * LPR);
+            // key differs from row r-1's (row -1: `cur`); every lane of the warp
+            // is here (full-warp ballot: a group mask costs a WARPSYNC loop)
+            const unsigned heads = __ballot_sync(0xffffffffu, li < cnt && kmine != kprev) >> (gi * LPR);
             if constexpr (SUB == RS) {
                 // the whole stage's rows into registers at once, then hand the buffer
                 // back to the TMA producer right away (the proxy fence orders these
@@ -565,10 +612,13 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
 #pragma unroll
                     for (int j = 0; j < VPL; ++j)
                         rows[r][j] = (r < cnt && col_ok[j]) ? lds_vec<Raw>(sbase + r * row_bytes + j * LPR * VB) : Raw{};
+                float wst[SUB];
+#pragma unroll
+                for (int r = 0; r < SUB; ++r) wst[r] = MODE == 2 ? wslots[r] : 1.0f;
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();
                 refill(s);
-                process(rows, heads, kmine, 0, cnt, r_base, wmine);
+                process(rows, heads, kmine, 0, cnt, r_base, wst);
             } else {
                 // large stages of small rows: SUB rows at a time, buffer released after
 #pragma unroll 1
@@ -581,7 +631,10 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
                             rows[r][j] = (r0 + r < cnt && col_ok[j])
                                              ? lds_vec<Raw>(sbase + (r0 + r) * row_bytes + j * LPR * VB)
                                              : Raw{};
-                    process(rows, heads >> r0, kmine, r0, cnt - r0, r_base + r0, wmine);
+                    float wst[SUB];
+#pragma unroll
+                    for (int r = 0; r < SUB; ++r) wst[r] = (MODE == 2 && r0 + r < RS) ? wslots[r0 + r] : 1.0f;
+                    process(rows, heads >> r0, kmine, r0, cnt - r0, r_base + r0, wst);
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();
@@ -620,10 +673,11 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
             const long long r_base = e_lo + (long long)s * RS;
             int cnt = (int)(e_hi - r_base);
             cnt = cnt < 0 ? 0 : (cnt > RS ? RS : cnt);
-            long long kprev = __shfl_up_sync(gmask, kmine, 1, LPR);
+            long long kprev = __shfl_up_sync(0xffffffffu, kmine, 1, LPR);
             if (li == 0) kprev = cur;
-            const unsigned heads = __ballot_sync(gmask, li < cnt && kmine != kprev) >> (gi * LPR);
-            process(rows, heads, kmine, 0, cnt, r_base, 1.0f);
+            const unsigned heads = __ballot_sync(0xffffffffu, li < cnt && kmine != kprev) >> (gi * LPR);
+            const float wst[SUB] = {};
+            process(rows, heads, kmine, 0, cnt, r_base, wst);
         }
     }
 
@@ -666,48 +720,43 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
     // agent's head partial, in agent order (deterministic), write the row once.
     if (nrows > 0 && (flags & TM_HEAD_OPEN) && !(flags & TM_MIDDLE)) {
         long long u = a - 1;
+        bool ok = true;
         for (; u >= 0; --u) {  // predecessors are consistent by construction: agent
                                // u's tail test and agent u+1's head test compare the same keys
-            while (ld_acquire_u64(&p.flag[u]) != pub) {
+            if (!wait_flag_or_poison(&p.flag[u], pub, p.ctrl)) {
+                ok = false;
+                break;
             }
             if (!(ld_volatile_i32(&p.meta[u].flags) & TM_MIDDLE)) break;
         }
         if (u < 0) u = 0;  // unreachable (agent 0 never has an open head)
-        const long long count = head_end - ld_volatile_i64(&p.meta[u].tail_start);
-        float tot[VPL][VW];
-#pragma unroll
-        for (int j = 0; j < VPL; ++j) {
-            const int v = vec_col(j);
-#pragma unroll
-            for (int q = 0; q < VW; ++q) tot[j][q] = (v < p.NV) ? ld_cg_f32(p.carry_t + u * (long long)F + v * VW + q) : 0.f;
-        }
-        for (long long m = u + 1; m < a; ++m) {
+        if (ok) {
+            const long long count = head_end - ld_volatile_i64(&p.meta[u].tail_start);
+            float tot[VPL][VW];
 #pragma unroll
             for (int j = 0; j < VPL; ++j) {
                 const int v = vec_col(j);
 #pragma unroll
-                for (int q = 0; q < VW; ++q)
-                    if (v < p.NV) tot[j][q] = fold<ISMAX>(tot[j][q], ld_cg_f32(p.carry_h + m * (long long)F + v * VW + q));
+                for (int q = 0; q < VW; ++q) tot[j][q] = (v < p.NV) ? ld_cg_f32(p.carry_t + u * (long long)F + v * VW + q) : 0.f;
             }
+            for (long long m = u + 1; m < a; ++m) {
+#pragma unroll
+                for (int j = 0; j < VPL; ++j) {
+                    const int v = vec_col(j);
+#pragma unroll
+                    for (int q = 0; q < VW; ++q)
+                        if (v < p.NV) tot[j][q] = fold<ISMAX>(tot[j][q], ld_cg_f32(p.carry_h + m * (long long)F + v * VW + q));
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < VPL; ++j)
+#pragma unroll
+                for (int q = 0; q < VW; ++q) tot[j][q] = fold<ISMAX>(tot[j][q], hacc[j][q]);
+            write_row(first_key, tot, count);
         }
-#pragma unroll
-        for (int j = 0; j < VPL; ++j)
-#pragma unroll
-            for (int q = 0; q < VW; ++q) tot[j][q] = fold<ISMAX>(tot[j][q], hacc[j][q]);
-        write_row(first_key, tot, count);
     }
     // ---- last CTA out re-arms the control words for the next call
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        const unsigned done = atomicAdd(&p.ctrl->done, 1u);
-        if (done == gridDim.x - 1) {
-            p.ctrl->done = 0;
-            p.ctrl->ticket = 0;
-            __threadfence();
-            atomicAdd(&p.ctrl->epoch, 1ull);
-        }
-    }
+    retire_cta(p.ctrl);
 }
 
 }  // namespace geot

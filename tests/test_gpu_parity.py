@@ -371,6 +371,31 @@ def test_fused_gather_stream_stress_and_weighted(geot, kind):
     check(yw.cpu().numpy(), refw, "sum", "f32", "real", what=f"weighted gather-stream {kind}")
 
 
+# every compiled gather pipeline (launch.cuh GEOT_GSHAPE) x weighted / unweighted,
+# integer-valued x and weights: bit-exact.  Covers both stage schedules (the
+# buffer refilled before the fold when RS <= 8, after it when RS = 12).
+GATHER_PIPES = {4: [(16, 4, 4)], 8: [(16, 6, 4), (16, 8, 3)], 16: [(16, 6, 4), (16, 8, 3), (16, 12, 2)],
+                32: [(16, 6, 4), (16, 8, 3), (16, 12, 2)]}
+
+
+@pytest.mark.parametrize("F", [16, 32, 64, 128])
+@pytest.mark.parametrize("weighted", [False, True])
+def test_gather_every_pipeline(geot, F, weighted):
+    V, E, S = 7_000, 180_001, 9_000
+    L, dst, src, x = fused_case(E, S, V, F, "f32", "int", "powerlaw15", F + 11)
+    w = np.random.default_rng(F).integers(-3, 4, size=E).astype(np.float32) if weighted else None
+    ref = oracle.gather_segment_reduce(x, src, dst, S, "sum", weight=w, nthreads=oracle.default_threads())
+    lpr = max(4, min(32, F // 4))
+    for (W, RS, NS) in GATHER_PIPES[lpr]:
+        for it in (torch.int32, torch.int64):
+            y = geot.geot_gather_segment_reduce(
+                torch.from_numpy(x).cuda(), torch.from_numpy(src).to(it).cuda(), torch.from_numpy(dst).to(it).cuda(),
+                S, "sum", weight=None if w is None else torch.from_numpy(w).cuda(),
+                cfg={"variant": 3, "warps_per_cta": W, "rows_per_group": RS, "stages": NS})
+            check(y.cpu().numpy(), ref, "sum", "f32", "int", counts=L,
+                  what=f"gather pipe F={F} ({W},{RS},{NS}) w={weighted} {it}")
+
+
 # ---------------------------------------------------------------- integer kernels
 def test_offsets_partition_validate(geot):
     for kind in synth.STRESS_KINDS:
@@ -480,3 +505,29 @@ def test_gather_backward_and_sddmm(geot, op, weighted):
         g = np.ones(E) if op == "sum" else 1.0 / np.bincount(dst, minlength=S)[dst]
         Aw = g * np.abs(x[src].astype(np.float64) * dY[dst]).sum(axis=1)
         assert np.all(np.abs(wt.grad.cpu().numpy().astype(np.float64) - dw_ref) <= 1e-5 * Aw)
+
+
+# ---------------------------------------------------------------- workspace poisoning
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("F,variant", [(128, 3), (1, 2)])
+def test_poisoned_workspace_recovers(geot, F, variant):
+    """A workspace whose control words are not at rest (here: a stale ticket)
+    must neither hang nor trap: the call retires, geot_workspace_status reports
+    the poison, and checked=True repairs the workspace and recomputes."""
+    E, S = 400_000, 30_000
+    L, idx, X = make_case(E, S, F, "f32", "int", "powerlaw", seed=12)
+    ref = oracle.segment_reduce(X, idx, S, "sum", nthreads=oracle.default_threads())
+    xt, it = to_torch_vals(X), torch.from_numpy(idx).to(torch.int32).cuda()
+    cfg = {"variant": variant}
+    geot.geot_segment_reduce(xt, it, S, "sum", cfg=cfg)
+    torch.cuda.synchronize()
+    key = (xt.device, torch.cuda.current_stream().cuda_stream)
+    assert geot.geot_workspace_check(repair=False)[key] == 0
+    geot._ws_cache[key].view(torch.int32)[0] = 7  # the ticket word of the control block
+    geot.geot_segment_reduce(xt, it, S, "sum", cfg=cfg)  # retires without output; must return
+    torch.cuda.synchronize()
+    assert geot.geot_workspace_check(repair=False)[key] & 1
+    y = geot.geot_segment_reduce(xt, it, S, "sum", cfg=cfg, checked=True)
+    torch.cuda.synchronize()
+    check(from_torch_vals(y), ref, "sum", "f32", "int", what="after repair")
+    assert geot.geot_workspace_check(repair=False)[key] == 0

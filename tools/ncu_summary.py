@@ -6,6 +6,10 @@ import subprocess
 import sys
 
 KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+        "sm__cycles_active.avg", "sm__cycles_elapsed.avg", "sm__cycles_active.min", "sm__cycles_active.max",
+        "lts__t_sectors_srcunit_tex_op_read_lookup_hit.sum", "lts__t_sectors_srcunit_tex_op_read.sum",
+        "lts__t_sector_hit_rate.pct", "l1tex__t_bytes.sum",
         "dram__throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_bytes.sum",
         "sm__throughput.avg.pct_of_peak_sustained_elapsed", "smsp__issue_active.avg.pct_of_peak_sustained_active",
         "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread", "launch__grid_size",
@@ -24,6 +28,8 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
 out = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hdr, units = rows[0], rows[1]
+extra = [h for h in hdr if ("dram__" in h and "pct" in h) or h.startswith("lts__t_bytes")]
+KEYS += [h for h in extra if h not in KEYS]
 for d in rows[2:]:
     print("==", d[hdr.index("Kernel Name")][:110])
     for k in KEYS:

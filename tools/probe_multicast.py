@@ -11,7 +11,7 @@ os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
 os.environ.setdefault("MASTER_PORT", "29533")
 dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
 print("has_multicast_support:", torch._C._distributed_c10d._SymmetricMemory.has_multicast_support(
-    torch._C._distributed_c10d.DeviceType.CUDA, 0))
+    symm_mem.DeviceType.CUDA, 0))
 try:
     t = symm_mem.empty((1024, 128), dtype=torch.float32, device="cuda")
     h = symm_mem.rendezvous(t, dist.group.WORLD.group_name)

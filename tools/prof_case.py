@@ -1,5 +1,5 @@
 """Run one configuration a few times (for ncu):
-python tools/prof_case.py E S F dtype dist [cfg-json|-] [fused|-] [op] [mode]"""
+python tools/prof_case.py E S F dtype dist [cfg-json|-] [fused|weighted|-] [op] [mode]"""
 import json
 import os
 import sys
@@ -14,7 +14,8 @@ import synth.device as sd  # noqa: E402
 E, S, F = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3])
 dt, dist = sys.argv[4], sys.argv[5]
 cfg = json.loads(sys.argv[6]) if len(sys.argv) > 6 and sys.argv[6] not in ("", "-") else None
-fused = len(sys.argv) > 7 and sys.argv[7] == "fused"
+fused = len(sys.argv) > 7 and sys.argv[7] in ("fused", "weighted")
+weighted = len(sys.argv) > 7 and sys.argv[7] == "weighted"
 op = sys.argv[8] if len(sys.argv) > 8 else "sum"
 mode = sys.argv[9] if len(sys.argv) > 9 else ("signed" if op == "max" else "real")
 tdt = torch.float32 if dt == "f32" else torch.bfloat16
@@ -23,7 +24,8 @@ idx = sd.index_from_lengths(L)
 if fused:
     x = sd.values(S, F, 5, dtype=tdt, mode=mode)
     src = sd.src_index(E, S, 1005)
-    run = lambda: geot.geot_gather_segment_reduce(x, src, idx, S, op, cfg=cfg)  # noqa: E731
+    w = sd.values(E, 1, 7, dtype=torch.float32)[:, 0].contiguous() if weighted else None
+    run = lambda: geot.geot_gather_segment_reduce(x, src, idx, S, op, weight=w, cfg=cfg)  # noqa: E731
 else:
     X = sd.values(E, F, 5, dtype=tdt, mode=mode)
     run = lambda: geot.geot_segment_reduce(X, idx, S, op, cfg=cfg)  # noqa: E731
