@@ -138,13 +138,30 @@ void geot_profile_events(cudaEvent_t before, cudaEvent_t after);
 geot_status geot_select_config(int64_t nnz, int64_t num_segments, int64_t F, geot_reduce op,
                                geot_dtype dtype, geot_itype itype, int fused, geot_config* cfg_out);
 
+/* geot_select_config with the north_star's skew feature: skew = the longest
+ * segment's length / (nnz / num_segments), e.g. from a plan computed once per
+ * graph (Python: paper_2404_03019_b200.geot_plan); skew <= 0 = unknown (what
+ * geot_select_config and the cfg = NULL reductions use).  NaN ->
+ * GEOT_ERR_INVALID_VALUE.  Pure host code. */
+geot_status geot_select_config_ex(int64_t nnz, int64_t num_segments, int64_t F, geot_reduce op,
+                                  geot_dtype dtype, geot_itype itype, int fused, double skew, geot_config* cfg_out);
+
+/* Diagnostics: the configuration the pre-refit hand rules pick (STREAM with the
+ * lane shape's default pipeline when eligible, else NARROW when eligible, else
+ * EDGE_TILE with ~128 KB tiles) — the baseline the refit tree is scored
+ * against (the paper's Fig. 6 comparison).  Pure host code. */
+geot_status geot_select_hand_rules(int64_t nnz, int64_t num_segments, int64_t F, geot_dtype dtype, int fused,
+                                   geot_config* cfg_out);
+
 /* The generated decision tree alone (select_tree.inc; Listing 5,
  * P:432-444), for diagnostics and the codegen-fidelity test: leaf tuple
  * (variant, rows_per_group, warps_per_cta, stages) for features
- * log2(nnz), avg = nnz/num_segments, F, dtype (0 f32 / 1 bf16), fused (0/1);
+ * log2(nnz), avg = nnz/num_segments, skew = log2(max length / avg) or -1 when
+ * unknown, F, dtype (0 f32 / 1 bf16), fused (0/1), op (0 sum / 1 mean / 2 max);
  * '<=' goes left at every threshold.  geot_select_config applies the leaf only
  * where it is valid for the input (else the hand rules). */
-void geot_select_tree(double log2_nnz, double avg, double F, double dtype, double fused, int32_t out[4]);
+void geot_select_tree(double log2_nnz, double avg, double skew, double F, double dtype, double fused, double op,
+                      int32_t out[4]);
 
 /* Provenance text of the compiled tree (perf DB, split, quality). */
 const char* geot_selector_provenance(void);

@@ -30,7 +30,7 @@ __all__ = [
     "geot_segment_reduce", "geot_gather_segment_reduce", "geot_gather_weight_segment_reduce",
     "geot_segment_offsets", "geot_validate_index", "geot_partition", "geot_select_config",
     "geot_workspace_size", "geot_launch_count", "geot_partition_exact", "geot_segment_reduce_split",
-    "geot_combine_partials", "geot_workspace_check", "segment_reduce", "index_segment_reduce",
+    "geot_combine_partials", "geot_workspace_check", "geot_plan", "segment_reduce", "index_segment_reduce",
     "index_weight_segment_reduce", "GeotConfig", "GeotError",
 ]
 
@@ -151,11 +151,25 @@ def geot_launch_count() -> int:
     return int(_L.geot_launch_count())
 
 
-def geot_select_config(nnz, num_segments, F, op="sum", dtype=torch.float32, itype=torch.int32, fused=False):
+def geot_select_config(nnz, num_segments, F, op="sum", dtype=torch.float32, itype=torch.int32, fused=False,
+                       skew=None):
+    """H2 selection (pure host).  skew = longest segment / (nnz / num_segments), when
+    known (geot_plan computes it once per graph); None = unknown."""
     c = GeotConfig()
-    _lib.check(_L.geot_select_config(nnz, num_segments, F, _op(op), _DT[dtype], _IT[itype], int(fused),
-                                     ctypes.byref(c)), "geot_select_config")
+    _lib.check(_L.geot_select_config_ex(nnz, num_segments, F, _op(op), _DT[dtype], _IT[itype], int(fused),
+                                        float(skew) if skew else 0.0, ctypes.byref(c)), "geot_select_config")
     return c
+
+
+def geot_plan(idx, num_segments, F, op="sum", dtype=torch.float32, fused=False):
+    """A cached plan for one graph: the segment-length skew measured once (one
+    offsets pass, one device->host read) and the configuration the selector
+    picks with it.  Pass the returned config as cfg= to the reductions."""
+    off = geot_segment_offsets(idx, num_segments)
+    E = idx.numel()
+    maxlen = int((off[1:] - off[:-1]).max().item()) if num_segments else 0
+    skew = maxlen / (E / max(num_segments, 1)) if E else 0.0
+    return geot_select_config(E, num_segments, F, op, dtype, idx.dtype, fused, skew=skew)
 
 
 def geot_workspace_size(nnz, num_segments, F, op="sum", dtype=torch.float32, itype=torch.int32, fused=False,

@@ -55,7 +55,9 @@ SIGNATURES = {
     "geot_workspace_size": ([_i64, _i64, _i64, _i32, _i32, _i32, _i32, _cfgp], _sz),
     "geot_workspace_init": ([_vp, _sz, _vp], _i32),
     "geot_workspace_status": ([_vp, _sz, _vp, ctypes.POINTER(ctypes.c_int32)], _i32),
-    "geot_select_tree": ([ctypes.c_double] * 5 + [ctypes.POINTER(ctypes.c_int32)], None),
+    "geot_select_config_ex": ([_i64, _i64, _i64, _i32, _i32, _i32, _i32, ctypes.c_double, _cfgp], _i32),
+    "geot_select_hand_rules": ([_i64, _i64, _i64, _i32, _i32, _cfgp], _i32),
+    "geot_select_tree": ([ctypes.c_double] * 7 + [ctypes.POINTER(ctypes.c_int32)], None),
     "geot_selector_provenance": ([], ctypes.c_char_p),
     "geot_segment_reduce": ([_vp, _vp, _i64, _i64, _i64, _i32, _i32, _i32, _vp, _vp, _sz, _vp], _i32),
     "geot_segment_reduce_ex": ([_vp, _vp, _i64, _i64, _i64, _i64, _i32, _i32, _i32, _vp, _vp, _sz, _cfgp, _vp],

@@ -150,7 +150,7 @@ static geot_status from_cuda(cudaError_t e) {
 static geot_status resolve_config(long long nnz, long long S, long long F, geot_reduce op, geot_dtype dt,
                                   geot_itype it, int fused, const geot_config* user, geot_config* out) {
     geot_config c;
-    geot_status st = select_config_impl(nnz, S, F, op, dt, it, fused, &c);
+    geot_status st = select_config_impl(nnz, S, F, op, dt, it, fused, 0.0, &c);
     if (st != GEOT_OK) return st;
     if (user) {
         if (user->reserved != 0) return GEOT_ERR_INVALID_VALUE;
@@ -439,9 +439,10 @@ int geot_abi_version(void) { return GEOT_ABI_VERSION; }
 
 uint64_t geot_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
-void geot_select_tree(double log2_nnz, double avg, double F, double dtype, double fused, int32_t out[4]) {
+void geot_select_tree(double log2_nnz, double avg, double skew, double F, double dtype, double fused, double op,
+                      int32_t out[4]) {
     int o[4];
-    select_tree_raw(log2_nnz, avg, F, dtype, fused, o);
+    select_tree_raw(log2_nnz, avg, skew, F, dtype, fused, op, o);
     for (int i = 0; i < 4; ++i) out[i] = o[i];
 }
 
@@ -462,7 +463,23 @@ geot_status geot_select_config(int64_t nnz, int64_t num_segments, int64_t F, geo
     geot_status st = check_enums(op, dtype, itype);
     if (st != GEOT_OK) return st;
     if (nnz < 0 || num_segments < 0 || F < 1) return GEOT_ERR_INVALID_VALUE;
-    return select_config_impl(nnz, num_segments, F, op, dtype, itype, fused, cfg_out);
+    return select_config_impl(nnz, num_segments, F, op, dtype, itype, fused, 0.0, cfg_out);
+}
+
+geot_status geot_select_hand_rules(int64_t nnz, int64_t num_segments, int64_t F, geot_dtype dtype, int fused,
+                                  geot_config* cfg_out) {
+    if (!cfg_out || (int)dtype < 0 || (int)dtype > 1 || nnz < 0 || num_segments < 0 || F < 1)
+        return GEOT_ERR_INVALID_VALUE;
+    return select_hand_rules(nnz, num_segments, F, dtype, fused, cfg_out);
+}
+
+geot_status geot_select_config_ex(int64_t nnz, int64_t num_segments, int64_t F, geot_reduce op, geot_dtype dtype,
+                                  geot_itype itype, int fused, double skew, geot_config* cfg_out) {
+    if (!cfg_out) return GEOT_ERR_INVALID_VALUE;
+    geot_status st = check_enums(op, dtype, itype);
+    if (st != GEOT_OK) return st;
+    if (nnz < 0 || num_segments < 0 || F < 1 || !(skew == skew)) return GEOT_ERR_INVALID_VALUE;
+    return select_config_impl(nnz, num_segments, F, op, dtype, itype, fused, skew, cfg_out);
 }
 
 size_t geot_workspace_size(int64_t nnz, int64_t num_segments, int64_t F, geot_reduce op, geot_dtype dtype,

@@ -1,7 +1,8 @@
 """Selector (H2) checks on the CPU: the generated if/else (select_tree.inc,
 compiled into libgeot) agrees with the exported tree on random features and at
-every exact threshold ('<=' goes left), and geot_select_config
-always returns a configuration the library compiled for the input."""
+every exact threshold ('<=' goes left), and geot_select_config(_ex)
+always returns a configuration the library compiled for the input (any skew
+hint, any op)."""
 import ctypes
 import json
 import math
@@ -41,16 +42,16 @@ def test_codegen_matches_tree(L):
     rng = np.random.default_rng(0)
     xs = []
     for _ in range(1000):
-        xs.append([rng.uniform(10, 28), rng.uniform(1, 200), float(rng.choice([1, 2, 3, 4, 8, 16, 31, 32, 64, 96,
-                                                                               128, 256, 512, 1024])),
-                   float(rng.integers(0, 2)), float(rng.integers(0, 2))])
+        xs.append([rng.uniform(10, 28), rng.uniform(1, 200), float(rng.choice([-1.0, rng.uniform(0, 14)])),
+                   float(rng.choice([1, 2, 3, 4, 8, 16, 31, 32, 64, 96, 128, 256, 512, 1024])),
+                   float(rng.integers(0, 2)), float(rng.integers(0, 2)), float(rng.integers(0, 3))])
     # exact thresholds and their neighbours
     feats = tree["features"]
     for node in tree["nodes"]:
         if "leaf" in node:
             continue
         for delta in (0.0, -1e-9, 1e-9):
-            base = [20.0, 7.0, 128.0, 0.0, 0.0]
+            base = [20.0, 7.0, 5.0, 128.0, 0.0, 0.0, 0.0]
             base[feats.index(node["feature"])] = node["threshold"] + delta
             xs.append(base)
     for x in xs:
@@ -75,7 +76,9 @@ def test_select_config_always_valid(L):
                 for avg in (1, 3, 7, 16, 100):
                     for fused in (0, 1):
                         S = max(1, nnz // avg)
-                        assert L.geot_select_config(nnz, S, F, 0, dt, 0, fused, ctypes.byref(c)) == 0
+                        skew = float([0.0, 1.0, 30.0, 3000.0][(nnz + F + avg) % 4])
+                        op = (F + avg) % 3
+                        assert L.geot_select_config_ex(nnz, S, F, op, dt, 0, fused, skew, ctypes.byref(c)) == 0
                         wide = 4 if dt == 0 else 8
                         if c.variant == 3:  # 16-byte lane vectors, 8/16/32 lanes per row
                             assert c.vec_elems == wide and c.lanes_per_row >= 4
@@ -94,3 +97,13 @@ def test_select_config_always_valid(L):
                             assert c.vec_elems in (1, wide) and F % c.vec_elems == 0
                             assert c.lanes_per_row & (c.lanes_per_row - 1) == 0
                         assert math.isfinite(c.rows_per_group)
+
+
+def test_select_config_ex_arguments(L):
+    from paper_2404_03019_b200._lib import GeotConfig
+    c = GeotConfig()
+    assert L.geot_select_config_ex(1 << 20, 1 << 16, 64, 0, 0, 0, 0, float("nan"), ctypes.byref(c)) == 1
+    assert L.geot_select_config_ex(1 << 20, 1 << 16, 64, 0, 0, 0, 0, -1.0, ctypes.byref(c)) == 0
+    d = GeotConfig()
+    assert L.geot_select_config(1 << 20, 1 << 16, 64, 0, 0, 0, 0, ctypes.byref(d)) == 0
+    assert c.as_dict() == d.as_dict()  # unknown skew == the plain call
