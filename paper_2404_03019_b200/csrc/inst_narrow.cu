@@ -44,12 +44,12 @@ static bool encode_rows(CUtensorMap* m, const void* base, long long nrows, int l
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <typename T, int F, int OP, bool I64>
-static cudaError_t run_narrow(NarrowParams p, int nsm, cudaStream_t st) {
+template <typename T, int F, int OP, bool I64, bool REP>
+static cudaError_t run_narrow_r(NarrowParams p, int nsm, cudaStream_t st) {
     constexpr int KSZ = I64 ? 8 : 4;
     constexpr int ITEMS = narrow_items(F, (int)sizeof(T), KSZ);
     constexpr int LBV = ITEMS * F * (int)sizeof(T), LBK = ITEMS * KSZ;
-    auto kern = narrow_kernel<T, F, ITEMS, OP, I64>;
+    auto kern = narrow_kernel<T, F, ITEMS, OP, I64, REP>;
     const size_t smem = narrow_smem_bytes(LBV, LBK);
     int occ = cached_occupancy(kern, kNarrowWarps * 32, smem);
     if (occ <= 0) return cudaErrorInvalidConfiguration;
@@ -72,6 +72,13 @@ static cudaError_t run_narrow(NarrowParams p, int nsm, cudaStream_t st) {
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) g_launches.fetch_add(1, std::memory_order_relaxed);
     return e;
+}
+
+// f4 replicas (outs.n > 1) get their own instantiations, so the single-output
+// kernel carries no per-store replica loop (a branch region per item at F = 1)
+template <typename T, int F, int OP, bool I64>
+static cudaError_t run_narrow(const NarrowParams& p, int nsm, cudaStream_t st) {
+    return p.outs.n > 1 ? run_narrow_r<T, F, OP, I64, true>(p, nsm, st) : run_narrow_r<T, F, OP, I64, false>(p, nsm, st);
 }
 
 template <typename T, int F>

@@ -202,7 +202,7 @@ __device__ __forceinline__ void warp_segscan(float (&sv)[F], bool& sf, long long
     }
 }
 
-template <typename T, int F, int ITEMS, int OP, bool I64>
+template <typename T, int F, int ITEMS, int OP, bool I64, bool REP = false>
 __global__ void __launch_bounds__(kNarrowWarps * 32, 2)
     narrow_kernel(const __grid_constant__ CUtensorMap tmv, const __grid_constant__ CUtensorMap tmk,
                   const NarrowParams p) {
@@ -216,6 +216,13 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, 2)
     constexpr int AREA_V = narrow_area(LBV);
     constexpr int STAGE = narrow_stage_bytes(LBV, LBK);
     using KT = typename std::conditional<I64, long long, int>::type;
+    constexpr int RB = F * ESZ;               // output row bytes
+    constexpr int WROWS = STAGE / RB;         // output-window rows (a stage buffer; >= CH + 1)
+    static_assert(WROWS >= CH + 1, "the output window must cover a chunk's rows");
+    // window mode for rows of <= 8 bytes and fp32 F = 4 (A/B on the F = 1..8
+    // sweep: F=1 power-law 59 -> 43 us, fp32 F=4 -2 %, bf16 F=8 +16 % -> off;
+    // 32-byte rows: few segments per chunk, and the extra live row spills)
+    constexpr bool WIN = RB <= 8 || (RB == 16 && ESZ == 4);
 
     extern __shared__ __align__(16) unsigned char smem_dyn[];
     // the swizzle pattern is a function of the shared address: 1024-byte align the rings
@@ -272,8 +279,13 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, 2)
         float z[F];
 #pragma unroll
         for (int f = 0; f < F; ++f) z[f] = 0.0f;
-        for (int d = 0; d < p.outs.n; ++d)
-            for (long long r = r0; r < r1; ++r) st_row<T, F>(static_cast<T*>(p.outs.ptr[d]) + (r - p.outs.row_off) * F, z);
+        if constexpr (REP) {
+            for (int d = 0; d < p.outs.n; ++d)
+                for (long long r = r0; r < r1; ++r)
+                    st_row<T, F>(static_cast<T*>(p.outs.ptr[d]) + (r - p.outs.row_off) * F, z);
+        } else {
+            for (long long r = r0; r < r1; ++r) st_row<T, F>(out0 + (r - seg_lo) * F, z);
+        }
     };
     // a store at key k (32-bit relative arithmetic for int32 keys; memory-safe)
     const KT kseg_lo = (KT)seg_lo;
@@ -294,8 +306,9 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, 2)
         for (int f = 0; f < F; ++f) o[f] = (OP == OP_MEAN) ? __fdiv_rn(v[f], (float)count) : v[f];
         if (ok) {
             st_row<T, F>(out0 + rel * F, o);
-            for (int d = 1; d < p.outs.n; ++d)  // replicas (f4): global row index
-                st_row<T, F>(static_cast<T*>(p.outs.ptr[d]) + ((long long)rel + seg_lo - p.outs.row_off) * F, o);
+            if constexpr (REP)  // replicas (f4): global row index
+                for (int d = 1; d < p.outs.n; ++d)
+                    st_row<T, F>(static_cast<T*>(p.outs.ptr[d]) + ((long long)rel + seg_lo - p.outs.row_off) * F, o);
         }
     };
 
@@ -402,13 +415,41 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, 2)
         const KT klast = k[ITEMS - 1];  // padded: the last valid key
         const bool last_ends = nv > 0 && klast != kn;
         const unsigned em = (hm >> 1) | ((unsigned)last_ends << (nv > 0 ? nv - 1 : 0));  // items ending a segment
-        // segments that start and end inside the lane: store now
+        // segments that start and end inside the lane
         const unsigned smk = em & ~((hm & (0u - hm)) - 1u);
+        // the chunk's last valid row and its key (the running key of the next chunk)
+        const unsigned vmask = __ballot_sync(0xffffffffu, nv > 0);
+        const int ll = 31 - __clz(vmask);
+        const KT kl = __shfl_sync(0xffffffffu, klast, ll);
+        // Output window (warp-uniform choice): every row this chunk finalises
+        // lies in [rkey, kl] — finished segments and the empty rows between
+        // them.  When that span fits in the stage buffer the chunk writes its
+        // finished rows into a zeroed shared-memory window (slot = key - rkey)
+        // and copies the window out with coalesced stores: empty segments cost
+        // nothing extra and no per-row global address is formed.  Otherwise
+        // (very sparse keys, all-singleton chunks at F >= 2, unsorted data) the
+        // rows are stored directly and gaps zero-filled lane by lane.
+        const bool win = WIN && (unsigned long long)((long long)kl - (long long)rkey) < (unsigned long long)WROWS;
+        T* const wrow = reinterpret_cast<T*>(smem_raw + (size_t)(warp * NS + b) * STAGE);  // window slot 0 = row rkey
+        const uint32_t wkey = (uint32_t)rkey;
+        auto wput = [&](bool pred, KT key, const float (&v)[F], int count) {
+            // clamped slot: memory-safe whatever the keys (the span test covers sorted data)
+            uint32_t slot = (uint32_t)key - wkey;
+            slot = slot < (uint32_t)WROWS ? slot : (uint32_t)(WROWS - 1);
+            float o[F];
 #pragma unroll
-        for (int i = 0; i < ITEMS; ++i) {
-            int cnt = 1;
-            if constexpr (OP == OP_MEAN) cnt = i + 1 - (31 - __clz(hm & ((2u << i) - 1u)));
-            store_at((smk >> i) & 1u, k[i], acc[i], cnt);  // predicated, no branch
+            for (int f = 0; f < F; ++f) o[f] = (OP == OP_MEAN) ? __fdiv_rn(v[f], (float)count) : v[f];
+            if (pred) st_row<T, F>(wrow + (size_t)slot * F, o);
+        };
+        bool wr_lo = false, wr_hi = false;  // this lane finalised row rkey / row kl (window mode)
+
+        if (!win) {
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i) {
+                int cnt = 1;
+                if constexpr (OP == OP_MEAN) cnt = i + 1 - (31 - __clz(hm & ((2u << i) - 1u)));
+                store_at((smk >> i) & 1u, k[i], acc[i], cnt);  // predicated, no branch
+            }
         }
         // the running segment ended exactly at the previous chunk's end
         if (lane == 0 && s > 0 && (hm & 1u)) {
@@ -416,17 +457,17 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, 2)
 #pragma unroll
                 for (int f = 0; f < F; ++f) hacc[f] = rc[f];
                 head_end = c0;
-            } else {
+            } else if (!win) {
                 store_at(true, rkey, rc, (int)((c0 - e_lo) - rpos));
             }
         }
 
-        // gaps (empty segments) or unsorted keys: a lane whose key span differs
-        // from its number of heads.  Such a lane finds its gap items from the
-        // keys in its registers (bit i: k[i] - k[i-1] > 1, k[-1] = kp) and
-        // zero-fills each gap, reading the two keys of a gap back from its ring
-        // slot (a dynamic item index; no local memory).  Lanes without gaps idle.
-        {
+        // gaps (empty segments) or unsorted keys outside window mode: a lane
+        // whose key span differs from its number of heads.  Such a lane finds
+        // its gap items from the keys in its registers (bit i: k[i] - k[i-1] > 1,
+        // k[-1] = kp) and zero-fills each gap, reading the two keys of a gap back
+        // from its ring slot (a dynamic item index; no local memory).
+        if (!win) {
             const bool gap = nv > 0 && (long long)klast - (long long)kp != (long long)__popc(hm);
             if (__any_sync(0xffffffffu, gap) && gap) {
                 unsigned gm = 0;
@@ -486,6 +527,9 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, 2)
         // ---- the segment continuing into the lane from the left: ends at item j
         const bool cont = nv > 0 && !(hm & 1u);
         const int j = hm ? (__ffs(hm) - 2) : (last_ends ? nv - 1 : -1);
+        bool cput = false;  // window mode: this lane finalises row k[0] with ctot
+        float ctot[F];
+        int ccnt = 1;
         if (cont && j >= 0) {
             // the lane's partial at item j (a dynamic index)
             float tot[F];
@@ -525,8 +569,54 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, 2)
 #pragma unroll
                 for (int f = 0; f < F; ++f) hacc[f] = tot[f];
                 head_end = r0 + j + 1;
-            } else {
+            } else if (!win) {
                 store_at(true, k[0], tot, (int)((r0 - e_lo) + j + 1 - cpos));
+            } else {
+                cput = true;
+#pragma unroll
+                for (int f = 0; f < F; ++f) ctot[f] = tot[f];
+                ccnt = (int)((r0 - e_lo) + j + 1 - cpos);
+            }
+        }
+
+        if (win) {
+            // rows finalised here: (rkey, kl) always; rkey if its segment (not the
+            // agent's head) ended in this chunk; kl if its segment ended at the
+            // agent's last row
+            const bool put0 = lane == 0 && s > 0 && (hm & 1u) && !rhead;  // running segment, ended at c0
+            wr_lo = put0 || (cput && k[0] == rkey);
+            wr_hi = (cput && k[0] == kl) || (lane == ll && nv > 0 && ((smk >> (nv - 1)) & 1u));
+            long long lo = (long long)rkey + (__any_sync(0xffffffffu, wr_lo) ? 0 : 1);
+            long long hi = (long long)kl - (__any_sync(0xffffffffu, wr_hi) ? 0 : 1);
+            if (lo < seg_lo) lo = seg_lo;
+            if (hi > seg_hi - 1) hi = seg_hi - 1;
+            using U = typename std::conditional<
+                RB >= 16, uint4,
+                typename std::conditional<RB == 8, uint2,
+                                          typename std::conditional<RB == 4, uint32_t, uint16_t>::type>::type>::type;
+            constexpr int UPR = RB / (int)sizeof(U);  // units per row
+            const int nunits = hi >= lo ? (int)(hi - lo + 1) * UPR : 0;
+            U* const wu = reinterpret_cast<U*>(wrow + (size_t)((uint32_t)lo - wkey) * F);
+            __syncwarp();  // every lane is done reading the stage (keys, values, partials)
+            for (int u = lane; u < nunits; u += 32) wu[u] = U{};
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i) {
+                int cnt = 1;
+                if constexpr (OP == OP_MEAN) cnt = i + 1 - (31 - __clz(hm & ((2u << i) - 1u)));
+                wput((smk >> i) & 1u, k[i], acc[i], cnt);
+            }
+            if (put0) wput(true, rkey, rc, (int)((c0 - e_lo) - rpos));
+            if (cput) wput(true, k[0], ctot, ccnt);
+            __syncwarp();
+            if constexpr (REP) {
+                for (int d = 0; d < p.outs.n; ++d) {
+                    U* const g = reinterpret_cast<U*>(static_cast<T*>(p.outs.ptr[d]) + (lo - p.outs.row_off) * F);
+                    for (int u = lane; u < nunits; u += 32) g[u] = wu[u];
+                }
+            } else {
+                U* const g = reinterpret_cast<U*>(out0 + (lo - seg_lo) * F);
+                for (int u = lane; u < nunits; u += 32) g[u] = wu[u];
             }
         }
 
@@ -537,11 +627,9 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, 2)
         if (lane == 0 && s + NS < nring) issue(s + NS);
 
         // ---- running segment for the next chunk: the last valid lane's state
-        const unsigned vmask = __ballot_sync(0xffffffffu, nv > 0);
-        const int ll = 31 - __clz(vmask);
 #pragma unroll
         for (int f = 0; f < F; ++f) rc[f] = __shfl_sync(0xffffffffu, sv[f], ll);
-        rkey = __shfl_sync(0xffffffffu, klast, ll);
+        rkey = kl;
         if constexpr (OP == OP_MEAN) rpos = __shfl_sync(0xffffffffu, spos, ll);
         if (__any_sync(0xffffffffu, hm != 0)) rhead = false;
     }
