@@ -314,8 +314,9 @@ static geot_status reduce_common(const void* X, long long V, const void* src_idx
         // the agents for that pipeline, not for the selected one
         if (os.n > 1 && mode == 0) stream_default_pipe(c.lanes_per_row, c.vecs_per_lane, &c.warps_per_cta,
                                                        &c.rows_per_group, &c.stages);
-        const long long NA =
+        long long NA =
             stream_agents(nnz, c.lanes_per_row, c.warps_per_cta, nsm, c.stages == 1 ? 2 : 1);  // LDG mode: 2 CTAs/SM
+        if (c.lanes_per_row <= 8 && S >= 0xFFFFFFFFLL) NA = 0;  // small-row path: 32-bit relative keys
         if (NA > 0) {
             const WsLayout L = ws_layout(NA, F);
             if (L.total > 0) {
@@ -337,6 +338,9 @@ static geot_status reduce_common(const void* X, long long V, const void* src_idx
             sp.seg_base = seg_base;
             sp.S = S;
             sp.NA = NA;
+            // L rows per agent, a multiple of RS (stream.cuh: agent ranges, 4+ agents per warp)
+            sp.L = ((nnz + NA - 1) / NA + c.rows_per_group - 1) / c.rows_per_group * c.rows_per_group;
+            sp.NF = nnz / sp.L;
             sp.F = (int)F;
             sp.NV = (int)(F / c.vec_elems);
             sp.RS = c.rows_per_group;

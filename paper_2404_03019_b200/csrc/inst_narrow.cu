@@ -27,35 +27,53 @@ static EncodeTiledFn encode_fn() {
     return fn;
 }
 
-// rows of LB bytes over [base, base + nrows*LB), box = 32 rows, swizzle = LB
-static bool encode_rows(CUtensorMap* m, const void* base, long long nrows, int lb) {
+bool encode_tensor_map(CUtensorMap* m, CUtensorMapDataType dt, int rank, const void* base, const cuuint64_t* dims,
+                       const cuuint64_t* strides, const cuuint32_t* box, CUtensorMapSwizzle sw) {
     EncodeTiledFn fn = encode_fn();
-    if (!fn || nrows < 32 || nrows > 0x7fffffffLL) return false;
-    const cuuint64_t dims[2] = {(cuuint64_t)lb, (cuuint64_t)nrows};
+    if (!fn) return false;
+    const cuuint32_t estr[5] = {1u, 1u, 1u, 1u, 1u};
+    return fn(m, dt, (cuuint32_t)rank, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// rows of LB bytes over [base, base + nrows*LB), box = `boxrows` rows, swizzle = LB
+// (rows over 256 bytes: 4-byte elements, the box's inner extent is <= 256 elements)
+static bool encode_rows(CUtensorMap* m, const void* base, long long nrows, int lb, int boxrows) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn || nrows < boxrows || nrows > 0x7fffffffLL || lb > 1024) return false;
+    const int esz = lb > 256 ? 4 : 1;
+    const cuuint64_t dims[2] = {(cuuint64_t)(lb / esz), (cuuint64_t)nrows};
     const cuuint64_t strides[1] = {(cuuint64_t)lb};
-    const cuuint32_t box[2] = {(cuuint32_t)lb, 32u};
+    const cuuint32_t box[2] = {(cuuint32_t)(lb / esz), (cuuint32_t)boxrows};
     const cuuint32_t estr[2] = {1u, 1u};
     const CUtensorMapSwizzle sw = lb == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
                                   : lb == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
                                   : lb == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
                                              : CU_TENSOR_MAP_SWIZZLE_NONE;
-    return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+    return fn(m, esz == 4 ? CU_TENSOR_MAP_DATA_TYPE_UINT32 : CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base),
+              dims, strides, box, estr,
               CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// rows of more than 32 bytes: LPR lane groups holding 16-byte slices, 8 (bf16: 4) rows per group
+template <typename T, int F>
+constexpr int narrow_lpr() { return F * (int)sizeof(T) > 32 ? F * (int)sizeof(T) / 16 : 1; }
+
 template <typename T, int F, int OP, bool I64, bool REP>
 static cudaError_t run_narrow_r(NarrowParams p, int nsm, cudaStream_t st) {
     constexpr int KSZ = I64 ? 8 : 4;
-    constexpr int ITEMS = narrow_items(F, (int)sizeof(T), KSZ);
-    constexpr int LBV = ITEMS * F * (int)sizeof(T), LBK = ITEMS * KSZ;
-    auto kern = narrow_kernel<T, F, ITEMS, OP, I64, REP>;
-    const size_t smem = narrow_smem_bytes(LBV, LBK);
+    constexpr int LPR = narrow_lpr<T, F>();
+    constexpr int NG = 32 / LPR;
+    constexpr int ITEMS = LPR > 1 ? (sizeof(T) == 2 ? 4 : 8) : narrow_items(F, (int)sizeof(T), KSZ);
+    constexpr int LBG = ITEMS * F * (int)sizeof(T), LBK = ITEMS * KSZ;
+    auto kern = narrow_kernel<T, F, ITEMS, OP, I64, REP, LPR>;
+    const size_t smem = narrow_smem_bytes(LBG, LBK, NG);
     int occ = cached_occupancy(kern, kNarrowWarps * 32, smem);
     if (occ <= 0) return cudaErrorInvalidConfiguration;
-    // every agent (warp) must own at least one chunk of 32*ITEMS rows
+    // every agent (warp) must own at least one chunk of NG*ITEMS rows
     long long grid = (long long)nsm * occ;
-    const long long max_agents = p.E / (32LL * ITEMS);
+    const long long max_agents = p.E / ((long long)NG * ITEMS);
     if (grid * kNarrowWarps > max_agents) grid = max_agents / kNarrowWarps;
     if (grid < 1) return cudaErrorNotSupported;
     p.NA = grid * kNarrowWarps;
@@ -64,7 +82,9 @@ static cudaError_t run_narrow_r(NarrowParams p, int nsm, cudaStream_t st) {
     memset(&tmv, 0, sizeof(tmv));
     memset(&tmk, 0, sizeof(tmk));
     const long long nrows = p.E / ITEMS;
-    p.tma = (LBV >= 16 && LBK >= 16 && encode_rows(&tmv, p.X, nrows, LBV) && encode_rows(&tmk, p.idx, nrows, LBK)) ? 1 : 0;
+    p.tma = (LBG >= 16 && LBK >= 16 && encode_rows(&tmv, p.X, nrows, LBG, NG) && encode_rows(&tmk, p.idx, nrows, LBK, NG))
+                ? 1
+                : 0;
     if (g_prof_before) cudaEventRecord(g_prof_before, st);
     kern<<<(unsigned)grid, kNarrowWarps * 32, smem, st>>>(tmv, tmk, p);
     if (g_prof_after) cudaEventRecord(g_prof_after, st);
@@ -96,8 +116,12 @@ static cudaError_t launch_narrow_t(const NarrowParams& p, int F, bool i64, int n
         case 2: return run_narrow_f<T, 2>(p, p.op, i64, nsm, st);
         case 4: return run_narrow_f<T, 4>(p, p.op, i64, nsm, st);
         case 8: return run_narrow_f<T, 8>(p, p.op, i64, nsm, st);
-        case 16:  // bf16 only (fp32 F = 16 measured 3x slower than the edge-tile kernel)
-            if constexpr (sizeof(T) == 2) return run_narrow_f<T, 16>(p, p.op, i64, nsm, st);
+        case 16:  // fp32: 4 lanes per row; bf16: one lane per row
+            return run_narrow_f<T, 16>(p, p.op, i64, nsm, st);
+        case 32:  // 8 (fp32) / 4 (bf16) lanes per row
+            return run_narrow_f<T, 32>(p, p.op, i64, nsm, st);
+        case 64:  // bf16: 8 lanes per row
+            if constexpr (sizeof(T) == 2) return run_narrow_f<T, 64>(p, p.op, i64, nsm, st);
             return cudaErrorNotSupported;
         default: return cudaErrorNotSupported;
     }

@@ -1,9 +1,12 @@
 // launch.cuh — host-side launchers of the kernel family (internal to libgeot).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstdlib>
+#include <cstring>
 #include <mutex>
 #include <unordered_map>
 
@@ -113,6 +116,11 @@ cudaError_t run_edge_tile(const EdgeTileParams& p, int ctas_per_sm, int nsm, cud
     return launch_fixup<T, ISMAX>(p, st);
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no swizzle
+// unless given, no interleave, 256-byte L2 promotion); false if unavailable.
+bool encode_tensor_map(CUtensorMap* m, CUtensorMapDataType dt, int rank, const void* base, const cuuint64_t* dims,
+                       const cuuint64_t* strides, const cuuint32_t* box, CUtensorMapSwizzle sw);
+
 // Stream kernel: one persistent CTA per SM (fewer when nnz is small so every
 // agent owns >= 1 row).  Agent count = carry slots.
 long long stream_agents(long long nnz, int lpr, int warps, int nsm, int ctas_per_sm);
@@ -128,8 +136,30 @@ cudaError_t run_stream(const StreamParams& p, const EdgeTileParams& fix, int nsm
     if (occ < (NS > 0 ? 1 : 2)) return cudaErrorInvalidConfiguration;  // agents assume this many CTAs/SM
     const long long grid = p.NA / ((long long)W * G);
     if (grid < 1 || grid * W * G != p.NA) return cudaErrorInvalidValue;
+    // the warp's value stages as one 3-D box: X viewed as [agent][stage][RS rows]
+    // (uint64 elements: the box's inner extent RS * row_bytes <= 2048 bytes)
+    StreamParams q = p;
+    CUtensorMap tmx;
+    std::memset(&tmx, 0, sizeof(tmx));
+    q.tma3 = 0;
+    static const bool no_tma3 = [] {  // experiments: GEOT_NO_TMA3=1 keeps the per-agent bulk copies
+        const char* e = std::getenv("GEOT_NO_TMA3");
+        return e && e[0] == '1';
+    }();
+    if constexpr (NS > 0 && MODE == 0 && G >= 4) {  // (stream.cuh EQL: equal-length agents)
+        const long long sb = (long long)RS * p.row_bytes;
+        if (!no_tma3 && p.NF >= 1 && sb % 16 == 0 && sb <= 2048 && p.L % RS == 0) {
+            const cuuint64_t dims[3] = {(cuuint64_t)(sb / 8), (cuuint64_t)(p.L / RS), (cuuint64_t)p.NF};
+            const cuuint64_t strides[2] = {(cuuint64_t)sb, (cuuint64_t)(p.L * p.row_bytes)};
+            const cuuint32_t box[3] = {(cuuint32_t)(sb / 8), 1u, (cuuint32_t)G};
+            q.tma3 = encode_tensor_map(&tmx, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, p.X, dims, strides, box,
+                                       CU_TENSOR_MAP_SWIZZLE_NONE)
+                         ? 1
+                         : 0;
+        }
+    }
     if (g_prof_before) cudaEventRecord(g_prof_before, st);
-    kern<<<(unsigned)grid, W * 32, smem, st>>>(p);
+    kern<<<(unsigned)grid, W * 32, smem, st>>>(q, tmx);
     if (g_prof_after) cudaEventRecord(g_prof_after, st);
     g_prof_before = g_prof_after = nullptr;
     cudaError_t e = cudaGetLastError();

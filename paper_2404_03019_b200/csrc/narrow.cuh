@@ -65,13 +65,17 @@ __host__ __device__ constexpr int narrow_items(int F, int esz, int ksz) {
     return r;
 }
 // one ring area (values or keys tile of 32 lane rows), 1024-byte aligned (swizzle atom)
-__host__ __device__ constexpr int narrow_area(int lb) { return ((32 * lb + 1023) / 1024) * 1024; }
-__host__ __device__ constexpr int narrow_stage_bytes(int lbv, int lbk) { return narrow_area(lbv) + narrow_area(lbk); }
+__host__ __device__ constexpr int narrow_area(int lb, int ng = 32) { return ((ng * lb + 1023) / 1024) * 1024; }
+__host__ __device__ constexpr int narrow_stage_bytes(int lbv, int lbk, int ng = 32) {
+    return narrow_area(lbv, ng) + narrow_area(lbk, ng);
+}
 // ring depth: 3 stages of <= 4 KB, else 2 (two 8-warp CTAs per SM fit either way)
-__host__ __device__ constexpr int narrow_stages(int lbv, int lbk) { return narrow_stage_bytes(lbv, lbk) <= 4096 ? 3 : 2; }
-__host__ __device__ constexpr size_t narrow_smem_bytes(int lbv, int lbk) {
-    return (size_t)kNarrowWarps * narrow_stages(lbv, lbk) * narrow_stage_bytes(lbv, lbk)  // rings
-           + (size_t)kNarrowWarps * narrow_stages(lbv, lbk) * 8                          // mbarriers
+__host__ __device__ constexpr int narrow_stages(int lbv, int lbk, int ng = 32) {
+    return narrow_stage_bytes(lbv, lbk, ng) <= 4096 ? 3 : 2;
+}
+__host__ __device__ constexpr size_t narrow_smem_bytes(int lbv, int lbk, int ng = 32) {
+    return (size_t)kNarrowWarps * narrow_stages(lbv, lbk, ng) * narrow_stage_bytes(lbv, lbk, ng)  // rings
+           + (size_t)kNarrowWarps * narrow_stages(lbv, lbk, ng) * 8                              // mbarriers
            + 1024;                                                                       // alignment slack
 }
 
@@ -183,10 +187,10 @@ __device__ __forceinline__ float nident() {
 // only while its own chain has not reached a segment start.  (Checked on every
 // non-decreasing 8-key sequence and on random 16/32-lane sequences by
 // geot_selftest_warp_segscan.)
-template <int F, int OP>
+template <int F, int OP, int LPR = 1>
 __device__ __forceinline__ void warp_segscan(float (&sv)[F], bool& sf, long long& spos, int lane) {
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
+    for (int d = LPR; d < 32; d <<= 1) {  // LPR lanes per row: a scan over the lane groups
         float ov[F];
 #pragma unroll
         for (int f = 0; f < F; ++f) ov[f] = __shfl_up_sync(0xffffffffu, sv[f], d);
@@ -202,21 +206,30 @@ __device__ __forceinline__ void warp_segscan(float (&sv)[F], bool& sf, long long
     }
 }
 
-template <typename T, int F, int ITEMS, int OP, bool I64, bool REP = false>
+// LPR > 1 (rows of 64 / 128 bytes): a row is LPR 16-byte lane slices and the
+// roles of a lane above are played by a group of LPR lanes: group g owns rows
+// g*ITEMS .. of the chunk, each lane its slice of them; the warp pass scans the
+// 32/LPR groups.  F is then the slice width (elements per lane), FR the row.
+template <typename T, int FR, int ITEMS, int OP, bool I64, bool REP = false, int LPR = 1>
 __global__ void __launch_bounds__(kNarrowWarps * 32, 2)
     narrow_kernel(const __grid_constant__ CUtensorMap tmv, const __grid_constant__ CUtensorMap tmk,
                   const NarrowParams p) {
-    constexpr int CH = 32 * ITEMS;        // rows per chunk
+    static_assert(FR % LPR == 0 && 32 % LPR == 0, "lane groups");
+    constexpr int F = FR / LPR;            // elements per lane of a row (a 16-byte slice when LPR > 1)
+    constexpr int NG = 32 / LPR;           // lane groups (row owners) per warp
+    constexpr int CH = NG * ITEMS;         // rows per chunk
     constexpr int ESZ = sizeof(T);
     constexpr int KSZ = I64 ? 8 : 4;
-    constexpr int LBV = ITEMS * F * ESZ;  // value bytes per lane per chunk
-    constexpr int LBK = ITEMS * KSZ;      // key bytes per lane per chunk
+    constexpr int LBV = ITEMS * F * ESZ;   // value bytes per lane per chunk
+    constexpr int LBG = ITEMS * FR * ESZ;  // value bytes per group per chunk (a TMA tile row)
+    constexpr int LBK = ITEMS * KSZ;       // key bytes per group per chunk
     constexpr int VWORDS = LBV / 4, KWORDS = LBK / 4;
-    constexpr int NS = narrow_stages(LBV, LBK);
-    constexpr int AREA_V = narrow_area(LBV);
-    constexpr int STAGE = narrow_stage_bytes(LBV, LBK);
+    constexpr int NS = narrow_stages(LBG, LBK, NG);
+    constexpr int AREA_V = narrow_area(LBG, NG);
+    constexpr int STAGE = narrow_stage_bytes(LBG, LBK, NG);
+    static_assert(LPR == 1 || F * ESZ == 16, "lane groups hold 16-byte slices");
     using KT = typename std::conditional<I64, long long, int>::type;
-    constexpr int RB = F * ESZ;               // output row bytes
+    constexpr int RB = FR * ESZ;              // output row bytes
     constexpr int WROWS = STAGE / RB;         // output-window rows (a stage buffer; >= CH + 1)
     static_assert(WROWS >= CH + 1, "the output window must cover a chunk's rows");
     // window mode for rows of <= 8 bytes and fp32 F = 4 (A/B on the F = 1..8
@@ -228,13 +241,15 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, 2)
     // the swizzle pattern is a function of the shared address: 1024-byte align the rings
     unsigned char* smem_raw = smem_dyn + ((1024u - (smem_u32(smem_dyn) & 1023u)) & 1023u);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int grp = lane / LPR, li = lane % LPR;  // row-owner group, slice within the row
     const uint32_t ring = smem_u32(smem_raw) + (uint32_t)(warp * NS * STAGE);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + (size_t)kNarrowWarps * NS * STAGE) + warp * NS;
 
     const T* __restrict__ X = static_cast<const T*>(p.X);
     const KT* __restrict__ I = static_cast<const KT*>(p.idx);
     const long long seg_lo = p.seg_base, seg_hi = p.seg_base + p.S;
-    T* __restrict__ out0 = static_cast<T*>(p.outs.ptr[0]) + (seg_lo - p.outs.row_off) * F;  // row of key seg_lo
+    // row of key seg_lo, this lane's slice
+    T* __restrict__ out0 = static_cast<T*>(p.outs.ptr[0]) + (seg_lo - p.outs.row_off) * FR + li * F;
     const long long E = p.E;
 
     __shared__ unsigned s_ticket;
@@ -264,7 +279,7 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, 2)
     auto issue = [&](int s) {  // lane 0: chunk s into stage s % NS
         const int b = s % NS;
         const int row = (int)((e_lo + (long long)s * CH) / ITEMS);  // lane-row coordinate
-        mbar_arrive_expect_tx(&bars[b], 32u * (LBV + LBK));
+        mbar_arrive_expect_tx(&bars[b], (uint32_t)NG * (LBG + LBK));
         tma_load_2d(ring + b * STAGE, &tmv, 0, row, &bars[b], pol);
         tma_load_2d(ring + b * STAGE + AREA_V, &tmk, 0, row, &bars[b], pol);
     };
@@ -282,9 +297,9 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, 2)
         if constexpr (REP) {
             for (int d = 0; d < p.outs.n; ++d)
                 for (long long r = r0; r < r1; ++r)
-                    st_row<T, F>(static_cast<T*>(p.outs.ptr[d]) + (r - p.outs.row_off) * F, z);
+                    st_row<T, F>(static_cast<T*>(p.outs.ptr[d]) + (r - p.outs.row_off) * FR + li * F, z);
         } else {
-            for (long long r = r0; r < r1; ++r) st_row<T, F>(out0 + (r - seg_lo) * F, z);
+            for (long long r = r0; r < r1; ++r) st_row<T, F>(out0 + (r - seg_lo) * FR, z);
         }
     };
     // a store at key k (32-bit relative arithmetic for int32 keys; memory-safe)
@@ -305,10 +320,11 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, 2)
 #pragma unroll
         for (int f = 0; f < F; ++f) o[f] = (OP == OP_MEAN) ? __fdiv_rn(v[f], (float)count) : v[f];
         if (ok) {
-            st_row<T, F>(out0 + rel * F, o);
+            st_row<T, F>(out0 + rel * FR, o);
             if constexpr (REP)  // replicas (f4): global row index
                 for (int d = 1; d < p.outs.n; ++d)
-                    st_row<T, F>(static_cast<T*>(p.outs.ptr[d]) + ((long long)rel + seg_lo - p.outs.row_off) * F, o);
+                    st_row<T, F>(static_cast<T*>(p.outs.ptr[d]) + ((long long)rel + seg_lo - p.outs.row_off) * FR + li * F,
+                                 o);
         }
     };
 
@@ -337,7 +353,7 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, 2)
 #pragma unroll 1
     for (int s = 0; s < nchunks; ++s) {
         const long long c0 = e_lo + (long long)s * CH;
-        const long long r0 = c0 + (long long)lane * ITEMS;  // this lane's first row
+        const long long r0 = c0 + (long long)grp * ITEMS;  // this lane's (group's) first row
         const bool last_chunk = s == nchunks - 1;  // warp-uniform
         const long long nvl = e_hi - r0;
         const int nv = nvl <= 0 ? 0 : (nvl >= ITEMS ? ITEMS : (int)nvl);  // valid items of the lane
@@ -349,8 +365,19 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, 2)
         if (p.tma) {
             mbar_wait(&bars[b], (uint32_t)((s / NS) & 1));
             uint32_t vw[VWORDS], kw[KWORDS];
-            lds_row<LBV>(ring + b * STAGE, lane, vw);
-            lds_row<LBK>(ring + b * STAGE + AREA_V, lane, kw);
+            if constexpr (LPR == 1) {
+                lds_row<LBV>(ring + b * STAGE, lane, vw);
+            } else {  // the lane's 16-byte slice of each of its group's rows
+#pragma unroll
+                for (int i = 0; i < ITEMS; ++i) {
+                    const uint4 v = lds_vec<uint4>(ring + b * STAGE + swz<LBG>((uint32_t)(grp * LBG + i * RB + li * 16)));
+                    vw[4 * i] = v.x;
+                    vw[4 * i + 1] = v.y;
+                    vw[4 * i + 2] = v.z;
+                    vw[4 * i + 3] = v.w;
+                }
+            }
+            lds_row<LBK>(ring + b * STAGE + AREA_V, grp, kw);
 #pragma unroll
             for (int i = 0; i < ITEMS; ++i) {
 #pragma unroll
@@ -367,7 +394,7 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, 2)
                 for (int i = 0; i < ITEMS; ++i) {
                     const bool ok = i < nv;
 #pragma unroll
-                    for (int f = 0; f < F; ++f) acc[i][f] = ok ? ld_elem<T>(X + (r0 + i) * F + f) : 0.f;
+                    for (int f = 0; f < F; ++f) acc[i][f] = ok ? ld_elem<T>(X + (r0 + i) * FR + li * F + f) : 0.f;
                     k[i] = ok ? __ldg(I + r0 + i) : (KT)0;
                 }
             }
@@ -386,10 +413,10 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, 2)
         // neighbours: the key before the lane's first row and after its last row
         // (lane 31 of a chunk that is not the agent's last: unknown -> "continues";
         // a segment ending there is stored by the next chunk's lane 0)
-        KT kp = __shfl_up_sync(0xffffffffu, k[ITEMS - 1], 1);
-        if (lane == 0) kp = rkey;
-        KT kn = __shfl_down_sync(0xffffffffu, k[0], 1);
-        if (lane == 31) kn = k[ITEMS - 1];
+        KT kp = __shfl_up_sync(0xffffffffu, k[ITEMS - 1], LPR);
+        if (grp == 0) kp = rkey;
+        KT kn = __shfl_down_sync(0xffffffffu, k[0], LPR);
+        if (grp == NG - 1) kn = k[ITEMS - 1];
         if (last_chunk && nv > 0 && r0 + nv >= e_hi) kn = knext_end;  // the agent's last row
 
         // ---- lane pass: heads (is_seg), sequential accumulation with restarts
@@ -431,6 +458,7 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, 2)
         // rows are stored directly and gaps zero-filled lane by lane.
         const bool win = WIN && (unsigned long long)((long long)kl - (long long)rkey) < (unsigned long long)WROWS;
         T* const wrow = reinterpret_cast<T*>(smem_raw + (size_t)(warp * NS + b) * STAGE);  // window slot 0 = row rkey
+        const int llg = ll / LPR;  // the chunk's last valid group
         const uint32_t wkey = (uint32_t)rkey;
         auto wput = [&](bool pred, KT key, const float (&v)[F], int count) {
             // clamped slot: memory-safe whatever the keys (the span test covers sorted data)
@@ -439,7 +467,7 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, 2)
             float o[F];
 #pragma unroll
             for (int f = 0; f < F; ++f) o[f] = (OP == OP_MEAN) ? __fdiv_rn(v[f], (float)count) : v[f];
-            if (pred) st_row<T, F>(wrow + (size_t)slot * F, o);
+            if (pred) st_row<T, F>(wrow + (size_t)slot * FR + li * F, o);
         };
         bool wr_lo = false, wr_hi = false;  // this lane finalised row rkey / row kl (window mode)
 
@@ -452,7 +480,7 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, 2)
             }
         }
         // the running segment ended exactly at the previous chunk's end
-        if (lane == 0 && s > 0 && (hm & 1u)) {
+        if (grp == 0 && s > 0 && (hm & 1u)) {
             if (rhead) {
 #pragma unroll
                 for (int f = 0; f < F; ++f) hacc[f] = rc[f];
@@ -481,11 +509,11 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, 2)
                     if (direct) return key_at(r0 + i);
                     if constexpr (I64) {
                         unsigned long long t;
-                        asm volatile("ld.shared.u64 %0, [%1];" : "=l"(t) : "r"(kb + swz<LBK>((uint32_t)(lane * LBK + i * 8))));
+                        asm volatile("ld.shared.u64 %0, [%1];" : "=l"(t) : "r"(kb + swz<LBK>((uint32_t)(grp * LBK + i * 8))));
                         return (long long)t;
                     } else {
                         int t;
-                        asm volatile("ld.shared.s32 %0, [%1];" : "=r"(t) : "r"(kb + swz<LBK>((uint32_t)(lane * LBK + i * 4))));
+                        asm volatile("ld.shared.s32 %0, [%1];" : "=r"(t) : "r"(kb + swz<LBK>((uint32_t)(grp * LBK + i * 4))));
                         return t;
                     }
                 };
@@ -503,7 +531,7 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, 2)
         for (int f = 0; f < F; ++f) sv[f] = acc[ITEMS - 1][f];
         bool sf = hm != 0;  // a segment starts in this lane (reset flag)
         long long spos = hm ? (r0 - e_lo) + (31 - __clz(hm)) : 0;  // start row of the lane's tail segment
-        warp_segscan<F, OP>(sv, sf, spos, lane);
+        warp_segscan<F, OP, LPR>(sv, sf, spos, lane);
         const bool reach = !sf;  // this lane's chain reaches back to the open segment
         if (reach) {
 #pragma unroll
@@ -513,11 +541,11 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, 2)
         // carry into this lane: the previous lane's inclusive value
         float cin[F];
 #pragma unroll
-        for (int f = 0; f < F; ++f) cin[f] = __shfl_up_sync(0xffffffffu, sv[f], 1);
+        for (int f = 0; f < F; ++f) cin[f] = __shfl_up_sync(0xffffffffu, sv[f], LPR);
         long long cpos = 0;
-        if constexpr (OP == OP_MEAN) cpos = __shfl_up_sync(0xffffffffu, spos, 1);
-        bool creach = __shfl_up_sync(0xffffffffu, (int)reach, 1) != 0;
-        if (lane == 0) {
+        if constexpr (OP == OP_MEAN) cpos = __shfl_up_sync(0xffffffffu, spos, LPR);
+        bool creach = __shfl_up_sync(0xffffffffu, (int)reach, LPR) != 0;
+        if (grp == 0) {
 #pragma unroll
             for (int f = 0; f < F; ++f) cin[f] = rc[f];
             cpos = rpos;
@@ -538,21 +566,25 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, 2)
                 // whose ring slot it has already consumed: write them there (same
                 // swizzled layout, conflict-free) and read item j back
                 const uint32_t vb = ring + b * STAGE;
+                // byte offset of the lane's element f of item i in the stage's value tile
+                auto voff = [&](int i, int f) -> uint32_t {
+                    if constexpr (LPR == 1)
+                        return swz<LBV>((uint32_t)(lane * LBV + (i * F + f) * 4));
+                    else
+                        return swz<LBG>((uint32_t)(grp * LBG + i * RB + li * 16 + f * 4));
+                };
 #pragma unroll
                 for (int q = 0; q < LBV / 16; ++q) {
-                    const uint32_t o = vb + swz<LBV>((uint32_t)(lane * LBV + q * 16));
-                    asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(o),
-                                 "f"(acc[(4 * q + 0) / F][(4 * q + 0) % F]), "f"(acc[(4 * q + 1) / F][(4 * q + 1) % F]),
-                                 "f"(acc[(4 * q + 2) / F][(4 * q + 2) % F]), "f"(acc[(4 * q + 3) / F][(4 * q + 3) % F])
+                    const int e0 = 4 * q;  // the lane's elements e0 .. e0+3 (item e0 / F)
+                    asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(vb + voff(e0 / F, e0 % F)),
+                                 "f"(acc[(e0 + 0) / F][(e0 + 0) % F]), "f"(acc[(e0 + 1) / F][(e0 + 1) % F]),
+                                 "f"(acc[(e0 + 2) / F][(e0 + 2) % F]), "f"(acc[(e0 + 3) / F][(e0 + 3) % F])
                                  : "memory");
                 }
 #pragma unroll
                 for (int f = 0; f < F; ++f) {
                     float t;
-                    asm volatile("ld.shared.f32 %0, [%1];"
-                                 : "=f"(t)
-                                 : "r"(vb + swz<LBV>((uint32_t)(lane * LBV + (j * F + f) * 4)))
-                                 : "memory");
+                    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(t) : "r"(vb + voff(j, f)) : "memory");
                     tot[f] = nfold<OP>(cin[f], t);
                 }
             } else {  // bf16: the partials are twice the row; select chain
@@ -583,9 +615,9 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, 2)
             // rows finalised here: (rkey, kl) always; rkey if its segment (not the
             // agent's head) ended in this chunk; kl if its segment ended at the
             // agent's last row
-            const bool put0 = lane == 0 && s > 0 && (hm & 1u) && !rhead;  // running segment, ended at c0
+            const bool put0 = grp == 0 && s > 0 && (hm & 1u) && !rhead;  // running segment, ended at c0
             wr_lo = put0 || (cput && k[0] == rkey);
-            wr_hi = (cput && k[0] == kl) || (lane == ll && nv > 0 && ((smk >> (nv - 1)) & 1u));
+            wr_hi = (cput && k[0] == kl) || (grp == llg && nv > 0 && ((smk >> (nv - 1)) & 1u));
             long long lo = (long long)rkey + (__any_sync(0xffffffffu, wr_lo) ? 0 : 1);
             long long hi = (long long)kl - (__any_sync(0xffffffffu, wr_hi) ? 0 : 1);
             if (lo < seg_lo) lo = seg_lo;
@@ -596,7 +628,7 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, 2)
                                           typename std::conditional<RB == 4, uint32_t, uint16_t>::type>::type>::type;
             constexpr int UPR = RB / (int)sizeof(U);  // units per row
             const int nunits = hi >= lo ? (int)(hi - lo + 1) * UPR : 0;
-            U* const wu = reinterpret_cast<U*>(wrow + (size_t)((uint32_t)lo - wkey) * F);
+            U* const wu = reinterpret_cast<U*>(wrow + (size_t)((uint32_t)lo - wkey) * FR);
             __syncwarp();  // every lane is done reading the stage (keys, values, partials)
             for (int u = lane; u < nunits; u += 32) wu[u] = U{};
             __syncwarp();
@@ -611,11 +643,11 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, 2)
             __syncwarp();
             if constexpr (REP) {
                 for (int d = 0; d < p.outs.n; ++d) {
-                    U* const g = reinterpret_cast<U*>(static_cast<T*>(p.outs.ptr[d]) + (lo - p.outs.row_off) * F);
+                    U* const g = reinterpret_cast<U*>(static_cast<T*>(p.outs.ptr[d]) + (lo - p.outs.row_off) * FR);
                     for (int u = lane; u < nunits; u += 32) g[u] = wu[u];
                 }
             } else {
-                U* const g = reinterpret_cast<U*>(out0 + (lo - seg_lo) * F);
+                U* const g = reinterpret_cast<U*>(out0 - li * F + (lo - seg_lo) * FR);
                 for (int u = lane; u < nunits; u += 32) g[u] = wu[u];
             }
         }
@@ -628,7 +660,7 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, 2)
 
         // ---- running segment for the next chunk: the last valid lane's state
 #pragma unroll
-        for (int f = 0; f < F; ++f) rc[f] = __shfl_sync(0xffffffffu, sv[f], ll);
+        for (int f = 0; f < F; ++f) rc[f] = __shfl_sync(0xffffffffu, sv[f], llg * LPR + li);
         rkey = kl;
         if constexpr (OP == OP_MEAN) rpos = __shfl_sync(0xffffffffu, spos, ll);
         if (__any_sync(0xffffffffu, hm != 0)) rhead = false;
@@ -638,7 +670,7 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, 2)
     if (hmk) {
         const int hl = __ffs(hmk) - 1;
 #pragma unroll
-        for (int f = 0; f < F; ++f) hacc[f] = __shfl_sync(0xffffffffu, hacc[f], hl);
+        for (int f = 0; f < F; ++f) hacc[f] = __shfl_sync(0xffffffffu, hacc[f], (hl / LPR) * LPR + li);
         head_end = __shfl_sync(0xffffffffu, head_end, hl);
     }
 
@@ -647,23 +679,26 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, 2)
     if (active) {
         const bool tail_open = nextk == (long long)rkey;
         if (head_open) flags |= TM_HEAD_OPEN;
-        if (e_hi == E && lane == 0 && (long long)rkey + 1 < seg_hi) gap_fill((long long)rkey, KEY_AFTER);
+        if (e_hi == E && grp == 0 && (long long)rkey + 1 < seg_hi) gap_fill((long long)rkey, KEY_AFTER);
         if (tail_open) {
             flags |= TM_TAIL_OPEN;
             if (rhead) flags |= TM_MIDDLE;  // the whole range lies inside one segment
-            if (lane == 0) {
-                float* c = (rhead ? p.carry_h : p.carry_t) + a * F;
+            if (grp == 0) {  // each lane of the first group writes its slice of the carry row
+                float* c = (rhead ? p.carry_h : p.carry_t) + a * FR + li * F;
 #pragma unroll
                 for (int f = 0; f < F; ++f) c[f] = rc[f];
-                p.meta[a].flags = flags;
-                p.meta[a].tail_start = e_lo + rpos;
+                if (lane == 0) {
+                    p.meta[a].flags = flags;
+                    p.meta[a].tail_start = e_lo + rpos;
+                }
                 __threadfence();
-                st_release_u64(&p.flag[a], pub);
             }
+            __syncwarp();
+            if (lane == 0) st_release_u64(&p.flag[a], pub);
         }
     }
     __syncwarp();
-    if (active && head_open && !(flags & TM_MIDDLE) && lane == 0) {
+    if (active && head_open && !(flags & TM_MIDDLE) && grp == 0) {
         long long u = a - 1;
         bool ok = true;
         for (; u >= 0; --u) {
@@ -677,10 +712,10 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, 2)
         if (ok) {
             float tot[F];
 #pragma unroll
-            for (int f = 0; f < F; ++f) tot[f] = ld_cg_f32(p.carry_t + u * F + f);
+            for (int f = 0; f < F; ++f) tot[f] = ld_cg_f32(p.carry_t + u * FR + li * F + f);
             for (long long m = u + 1; m < a; ++m)
 #pragma unroll
-                for (int f = 0; f < F; ++f) tot[f] = nfold<OP>(tot[f], ld_cg_f32(p.carry_h + m * F + f));
+                for (int f = 0; f < F; ++f) tot[f] = nfold<OP>(tot[f], ld_cg_f32(p.carry_h + m * FR + li * F + f));
 #pragma unroll
             for (int f = 0; f < F; ++f) tot[f] = nfold<OP>(tot[f], hacc[f]);
             store_at(true, (KT)first_key, tot, (int)(head_end - ld_volatile_i64(&p.meta[u].tail_start)));

@@ -21,6 +21,10 @@
 //    carry_fixup_kernel (edge_tile.cuh).
 #pragma once
 
+#include <cuda.h>
+
+#include <type_traits>
+
 #include "common.cuh"
 #include "edge_tile.cuh"
 
@@ -108,6 +112,9 @@ struct StreamParams {
     StreamCtrl* ctrl;
     long long E, seg_base, S;
     long long NA;      // agents (= carry slots)
+    long long L;       // rows per agent (a multiple of RS): agent a owns [a*L, min((a+1)*L, E))
+    long long NF;      // agents whose range is full (a*L + L <= E)
+    int tma3;          // 1: `tmx` is a valid 3-D tensor map of X as [agent][stage][RS rows]
     int F, NV;         // elements / 16-byte vectors per row
     int RS;            // rows per group per stage (== the kernel's RS)
     int row_bytes;     // F * sizeof(T)
@@ -125,6 +132,16 @@ __host__ __device__ inline size_t stream_smem_bytes(int W, int NS, int G, int RS
            + (size_t)W * NS * 8                      // mbarriers
            + (mode == 2 ? (size_t)W * NS * G * RS * 4 : 0)   // weight ring
            + (mode >= 1 ? (size_t)W * NS * G * RS * 8 : 0);  // src-id ring (NS stages ahead)
+}
+
+// 3-D tensor TMA (box {c0, c1, c2}) global -> shared, completing on `bar`
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            uint64_t* bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
 }
 
 // cp.async of 16 bytes; src_bytes 0 zero-fills the destination (no global read)
@@ -147,7 +164,8 @@ __device__ __forceinline__ void cp_async_16_zfill(uint32_t dst, const void* src,
 // are unspecified).
 template <typename T, int VW, int LPR, int VPL, bool ISMAX, int W, int RS, int NS, int MODE = 0, bool SRC64 = false,
           bool REP = false>
-__global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const StreamParams p) {
+__global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2)
+    stream_kernel(const StreamParams p, const __grid_constant__ CUtensorMap tmx) {
     constexpr bool TMA = NS > 0;
     static_assert(MODE == 0 || NS > 0, "the fused forms use the shared-memory ring");
     constexpr int NSX = TMA ? NS : 1;
@@ -197,24 +215,56 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
     }
     const unsigned long long pub = s_epoch + 1;  // "published in this call" flag value
 
-    // agent ranges (one 64-bit division per agent, once)
+    // agent ranges.  4+ agents per warp (EQL): L rows each (L = ceil(E / NA)
+    // rounded up to RS), so every stage of a full agent holds RS rows and the G
+    // agents of a warp sit at a constant stride in X (one 3-D TMA copy per stage,
+    // below); the last agents may be short or empty (empty ones only at the end:
+    // no agent ever waits on one).  Otherwise [a*E/NA, (a+1)*E/NA) (A/B: the
+    // equal-length split with per-agent copies cost products bf16 ~10 %).
+    constexpr bool EQL = TMA && MODE == 0 && G >= 4;
     const long long a = ((long long)s_ticket * W + warp) * G + gi;
-    const long long e_lo = (a * p.E) / p.NA;
-    const long long e_hi = ((a + 1) * p.E) / p.NA;
+    long long e_lo, e_hi;
+    if constexpr (EQL) {
+        e_lo = (a * p.L < p.E) ? a * p.L : p.E;
+        e_hi = (e_lo + p.L < p.E) ? e_lo + p.L : p.E;
+    } else {
+        e_lo = (a * p.E) / p.NA;
+        e_hi = ((a + 1) * p.E) / p.NA;
+    }
     const int nrows = (int)(e_hi - e_lo);
     const int nst = (nrows + RS - 1) / RS;
     const int nst_w = __reduce_max_sync(0xffffffffu, nst);
     const int nfull_w = __reduce_min_sync(0xffffffffu, nrows / RS);  // stages full in every group
-    long long glo[G], ghi[G];  // every group's range, for the producer lane
+    // every group's range, for the producer lane: held in registers for 1-2
+    // agents per warp; recomputed where used for EQL (4G registers otherwise)
+    const long long wa0 = ((long long)s_ticket * W + warp) * G;
+    constexpr int GH = EQL ? 1 : G;
+    long long glo_r[GH], ghi_r[GH];
+    const unsigned char* xg_r[GH];
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-        glo[g] = __shfl_sync(0xffffffffu, e_lo, g * LPR);
-        ghi[g] = __shfl_sync(0xffffffffu, e_hi, g * LPR);
+    for (int g = 0; g < GH; ++g) {
+        glo_r[g] = __shfl_sync(0xffffffffu, e_lo, g * LPR);
+        ghi_r[g] = __shfl_sync(0xffffffffu, e_hi, g * LPR);
+        xg_r[g] = reinterpret_cast<const unsigned char*>(X) + glo_r[g] * (long long)row_bytes;
     }
-
-    const unsigned char* xg[G];  // first row of every group's range (bytes)
-#pragma unroll
-    for (int g = 0; g < G; ++g) xg[g] = reinterpret_cast<const unsigned char*>(X) + glo[g] * (long long)row_bytes;
+    auto glo = [&](int g) -> long long {
+        if constexpr (EQL)
+            return (wa0 + g) * p.L < p.E ? (wa0 + g) * p.L : p.E;
+        else
+            return glo_r[g];
+    };
+    auto ghi = [&](int g) -> long long {
+        if constexpr (EQL)
+            return glo(g) + p.L < p.E ? glo(g) + p.L : p.E;
+        else
+            return ghi_r[g];
+    };
+    auto xg = [&](int g) -> const unsigned char* {
+        if constexpr (EQL)
+            return reinterpret_cast<const unsigned char*>(X) + glo(g) * (long long)row_bytes;
+        else
+            return xg_r[g];
+    };
 
     if constexpr (TMA) {
         // int32 keys land in the low half of 8-byte slots: zero the ring once
@@ -227,6 +277,12 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
         __syncwarp();
     }
     const uint64_t pol = policy_evict_first();
+    // 3-D TMA for the warp's value stages (G >= 2 agents per warp, plain form):
+    // every agent of the warp full, stage buffers 128-byte aligned
+    const long long a0 = wa0;  // the warp's first agent
+    bool use3d = false;
+    if constexpr (EQL)
+        use3d = p.tma3 && a0 + G <= p.NF && ((smem_u32(wbuf) | (uint32_t)stage_bytes) & 127u) == 0;
 
     const bool col_ok0 = li < p.NV;  // (fused forms: one 16-byte vector per lane)
     const unsigned long long xrows = (unsigned long long)p.V;
@@ -279,6 +335,11 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
                 const long long e = e_lo + (long long)s * RS + li;
                 if (li < RS && e < e_hi) cp_async_4(wring + (b * G + gi) * RS + li, p.w + e);
             }
+        } else if (lane == 0 && s < nfull_w && use3d) {
+            // all G agents of the warp are full: their stage-s rows are ONE box of
+            // the 3-D view [agent][stage][RS rows] of X (one TMA instead of G copies)
+            mbar_arrive_expect_tx(&bars[b], (uint32_t)stage_bytes);
+            tma_load_3d(smem_u32(wbuf + b * stage_bytes), &tmx, 0, s, (int)a0, &bars[b], pol);
         } else if (lane == 0 && s < nfull_w) {
             // every group has RS rows in this stage (all but the last stage or two)
             unsigned char* buf = wbuf + b * stage_bytes;
@@ -286,14 +347,15 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
             mbar_arrive_expect_tx(&bars[b], G * gb);
             const size_t soff = (size_t)s * gb;
 #pragma unroll
-            for (int g = 0; g < G; ++g) bulk_g2s(buf + g * gb, xg[g] + soff, gb, &bars[b], pol);
+            for (int g = 0; g < G; ++g)
+                bulk_g2s(buf + g * gb, xg(g) + soff, gb, &bars[b], pol);
         } else if (lane == 0) {
             unsigned char* buf = wbuf + b * stage_bytes;
             uint32_t total = 0;
             int cnt[G];
 #pragma unroll
             for (int g = 0; g < G; ++g) {
-                long long c = ghi[g] - (glo[g] + (long long)s * RS);
+                long long c = ghi(g) - (glo(g) + (long long)s * RS);
                 c = c < 0 ? 0 : (c > RS ? RS : c);
                 cnt[g] = (int)c;
                 total += (uint32_t)c * row_bytes;
@@ -302,7 +364,7 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
 #pragma unroll
             for (int g = 0; g < G; ++g)
                 if (cnt[g] > 0)
-                    bulk_g2s(buf + g * RS * row_bytes, X + (glo[g] + (long long)s * RS) * F,
+                    bulk_g2s(buf + g * RS * row_bytes, X + (glo(g) + (long long)s * RS) * F,
                              (uint32_t)cnt[g] * row_bytes, &bars[b], pol);
         }
         const long long e = e_lo + (long long)s * RS + li;
@@ -431,6 +493,12 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
     // bf16 max (branchy path): fold packed bf16 pairs with HMNMX2 (exact: the max is
     // one of the inputs) and widen to the fp32 acc only where a segment ends
     constexpr bool PKMAX = ISMAX && sizeof(T) == 2 && MODE == 0 && G < 4;
+    // the lean row loop (process_small below) for 4+ agents per warp.  (Also
+    // tried for every one-vector-per-lane shape: A/B on one box, products bf16
+    // 2810 -> 3482 us, arxiv 167 -> 191, Reddit fused 3693 -> 5495, fp32 F=64
+    // 850 -> 790: with 1-2 agents per warp the branchy end-of-segment path is
+    // cheaper than a predicated store + selects on every row.)
+    constexpr bool LEAN = G >= 4;
     constexpr int PKW = PKMAX ? VW / 2 : 1;
     uint32_t pk[VPL][PKW];
 #pragma unroll
@@ -579,6 +647,106 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
         }
     };
 
+    // ---- small rows (G >= 4 agents per warp, one 16-byte vector per lane): the
+    // per-row work of every agent is one predicated vector store of the segment
+    // that ended, selects and a packed fold; everything else is per stage —
+    // relative 32-bit keys, the gap test of every row (rare zero-fill), and the
+    // capture of the agent's head partial (at most once per agent)
+    // rows[r] is row koff + r of the stage (a sub-chunk of SUB rows; the stage's
+    // keys sit one per lane: lane li holds row li); heads_w is the group's head
+    // mask shifted by koff, cnt the group's valid rows counted from koff
+    auto process_small = [&](const Raw (&rows)[SUB][VPL], unsigned heads_w, long long kmine, long long kprev,
+                             int koff, int cnt, long long r_base, const float (&wst)[SUB]) {
+        // this sub-chunk's head bits (the shifted ballot still holds later rows and groups)
+        const unsigned heads = heads_w & ((1u << SUB) - 1u);
+        const unsigned long long nseg = (unsigned long long)p.S;  // < 2^32 - 1 (host check)
+        const int rb = (int)(r_base - e_lo);                      // agent-relative row of row 0
+        unsigned crel = (unsigned long long)(cur - seg_lo) < nseg ? (unsigned)(cur - seg_lo) : 0xFFFFFFFFu;
+        const unsigned krl = (unsigned long long)(kmine - seg_lo) < nseg ? (unsigned)(kmine - seg_lo) : 0xFFFFFFFFu;
+        int sst = (int)(seg_start - e_lo);
+        // empty segments before a head row (its key is not the previous key + 1),
+        // for the whole stage at its first sub-chunk
+        const bool gpl = koff == 0 && li < cnt && kmine != kprev && kmine != kprev + 1;
+        if (__any_sync(0xffffffffu, gpl)) {
+#pragma unroll 1
+            for (int r = 0; r < RS; ++r) {
+                const long long kp_ = __shfl_sync(0xffffffffu, kprev, r, LPR);
+                const long long k_ = __shfl_sync(0xffffffffu, kmine, r, LPR);
+                const bool g_ = __shfl_sync(0xffffffffu, (int)gpl, r, LPR) != 0;
+                if (g_) gap_fill(kp_, k_);
+            }
+        }
+        unsigned char* const out_lane = reinterpret_cast<unsigned char*>(out + li * VW);
+        const unsigned rowb = (unsigned)row_bytes;
+        auto rows_loop = [&](auto capc) {
+            constexpr bool CAP = decltype(capc)::value;
+            bool capp = first && head_open;  // the agent's head segment not closed yet
+#pragma unroll
+            for (int r = 0; r < SUB; ++r) {
+                const bool h = (heads >> r) & 1u;
+                const unsigned kr = __shfl_sync(0xffffffffu, krl, koff + r, LPR);
+                bool st = h && crel != 0xFFFFFFFFu && col_ok0;
+                if constexpr (CAP) {
+                    const bool hf = h && capp;
+                    if (hf) {
+#pragma unroll
+                        for (int q = 0; q < VW; ++q) hacc[0][q] = acc[0][q];
+                        flags |= TM_HEAD_OPEN;
+                        head_end = r_base + r;
+                    }
+                    st = st && !hf;
+                    capp = capp && !h;
+                }
+                {  // the segment crel ended at row r - 1: one predicated store
+                    float o[VW];
+#pragma unroll
+                    for (int q = 0; q < VW; ++q) o[q] = finalize(acc[0][q], p.op, rb + r - sst);
+                    const Raw pk = Cv::pack(o);
+                    if (st) st_vec(reinterpret_cast<Raw*>(out_lane + (size_t)crel * rowb), pk);
+                    if constexpr (REP) {
+                        if (st)
+                            for (int d = 1; d < p.outs.n; ++d) {
+                                T* rp = static_cast<T*>(p.outs.ptr[d]) +
+                                        ((long long)crel + seg_lo - p.outs.row_off) * (long long)F + li * VW;
+                                st_vec(reinterpret_cast<Raw*>(rp), pk);
+                            }
+                    }
+                }
+                crel = h ? kr : crel;
+                sst = h ? rb + r : sst;
+                float f[VW];
+                Cv::unpack(rows[r][0], f);
+                if constexpr (MODE == 2) {
+#pragma unroll
+                    for (int q = 0; q < VW; ++q) f[q] = (r < cnt ? wst[r] : 0.f) * f[q];  // stale weight slots past cnt
+                }
+                if constexpr (ISMAX) {
+                    const bool valid = r < cnt;
+#pragma unroll
+                    for (int q = 0; q < VW; ++q) acc[0][q] = h ? f[q] : (valid ? fmaxf(acc[0][q], f[q]) : acc[0][q]);
+                } else {  // rows past cnt are zero vectors (no head): adding them is exact
+#pragma unroll
+                    for (int q = 0; q < VW; q += 2) {
+                        const float2 t = __fadd2_rn(make_float2(h ? 0.f : acc[0][q], h ? 0.f : acc[0][q + 1]),
+                                                    make_float2(f[q], f[q + 1]));
+                        acc[0][q] = t.x;
+                        acc[0][q + 1] = t.y;
+                    }
+                }
+            }
+        };
+        if (__any_sync(0xffffffffu, first && head_open && heads != 0))
+            rows_loop(std::true_type{});
+        else
+            rows_loop(std::false_type{});
+        // running segment after the stage: the key of the group's last row
+        const int nv = cnt < SUB ? cnt : SUB;
+        const long long klast = __shfl_sync(0xffffffffu, kmine, koff + (nv > 0 ? nv - 1 : 0), LPR);
+        if (nv > 0) cur = klast;
+        seg_start = e_lo + sst;
+        first = first && heads == 0;
+    };
+
     if constexpr (TMA) {
         // refill the buffer of stage s with stage s + NS (fused: src ids from the queue)
         auto refill = [&](int s) {
@@ -618,11 +786,16 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();
                 refill(s);
-                process(rows, heads, kmine, 0, cnt, r_base, wst);
+                if constexpr (LEAN)
+                    process_small(rows, heads, kmine, kprev, 0, cnt, r_base, wst);
+                else
+                    process(rows, heads, kmine, 0, cnt, r_base, wst);
             } else {
                 // large stages of small rows: SUB rows at a time, buffer released after
+                // (the lean loop holds full-warp collectives: a warp-uniform bound)
+                const int cnt_loop = LEAN ? __reduce_max_sync(0xffffffffu, cnt) : cnt;
 #pragma unroll 1
-                for (int r0 = 0; r0 < cnt; r0 += SUB) {
+                for (int r0 = 0; r0 < cnt_loop; r0 += SUB) {
                     Raw rows[SUB][VPL];
 #pragma unroll
                     for (int r = 0; r < SUB; ++r)
@@ -634,7 +807,10 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
                     float wst[SUB];
 #pragma unroll
                     for (int r = 0; r < SUB; ++r) wst[r] = (MODE == 2 && r0 + r < RS) ? wslots[r0 + r] : 1.0f;
-                    process(rows, heads >> r0, kmine, r0, cnt - r0, r_base + r0, wst);
+                    if constexpr (LEAN)
+                        process_small(rows, heads >> r0, kmine, kprev, r0, cnt - r0, r_base + r0, wst);
+                    else
+                        process(rows, heads >> r0, kmine, r0, cnt - r0, r_base + r0, wst);
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();
@@ -677,7 +853,10 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2) stream_kernel(const St
             if (li == 0) kprev = cur;
             const unsigned heads = __ballot_sync(0xffffffffu, li < cnt && kmine != kprev) >> (gi * LPR);
             const float wst[SUB] = {};
-            process(rows, heads, kmine, 0, cnt, r_base, wst);
+            if constexpr (LEAN)
+                process_small(rows, heads, kmine, kprev, 0, cnt, r_base, wst);
+            else
+                process(rows, heads, kmine, 0, cnt, r_base, wst);
         }
     }
 

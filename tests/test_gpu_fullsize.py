@@ -29,10 +29,15 @@ def sample_segments(L, E, rng, n_random=4000, n_long=50):
     bounds = synth.lengths_to_bounds(L)
     picks = set(rng.choice(S, size=min(n_random, S), replace=False).tolist())
     picks |= set(np.argsort(L)[-n_long:].tolist())
-    for NA in (1184, 2368, 4736, 9472):  # agent splits of the stream/narrow kernels
+    for NA in (1184, 2368, 4736, 9472):  # agent splits of the narrow kernel (ITEMS-aligned k*E/NA)
         for k in range(1, NA):
             e = (k * E) // NA
             picks.add(int(np.searchsorted(bounds, e, side="right") - 1))
+    for NA in (2368, 4736, 9472, 18944):  # stream kernel: L = ceil(E/NA) rounded up to RS rows per agent
+        for RS in (4, 6, 12):
+            Lr = (-(-E // NA) + RS - 1) // RS * RS
+            e = np.arange(Lr, E, Lr)
+            picks.update((np.searchsorted(bounds, e, side="right") - 1).tolist())
     for tile in (256, 1024, 4096):  # edge-tile kernel tiles (a subset)
         for e in range(tile, E, max(tile, E // 3000)):
             picks.add(int(np.searchsorted(bounds, e, side="right") - 1))

@@ -174,7 +174,9 @@ NARROW = 2  # GEOT_VARIANT_NARROW
 
 
 @pytest.mark.parametrize("F,dtype", [(1, "f32"), (2, "f32"), (4, "f32"), (8, "f32"), (1, "bf16"), (2, "bf16"),
-                                     (4, "bf16"), (8, "bf16"), (16, "bf16")])
+                                     (4, "bf16"), (8, "bf16"), (16, "bf16"),
+                                     # lane groups: rows of 64 / 128 bytes as 16-byte lane slices
+                                     (16, "f32"), (32, "f32"), (32, "bf16"), (64, "bf16")])
 @pytest.mark.parametrize("op", ["sum", "mean", "max"])
 def test_narrow_variant(geot, F, dtype, op):
     for mode in ("real", "int"):
@@ -184,7 +186,7 @@ def test_narrow_variant(geot, F, dtype, op):
 @pytest.mark.parametrize("kind", synth.STRESS_KINDS)
 @pytest.mark.parametrize("itype", ["i32", "i64"])
 def test_narrow_stress(geot, kind, itype):
-    for F in (1, 4, 8):
+    for F in (1, 4, 8, 16, 32):
         for op in ("sum", "mean", "max"):
             parity(geot, 150_001, 12_000, F, op, "f32", "int", kind, seed=5, itype=itype, cfg={"variant": NARROW})
 

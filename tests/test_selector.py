@@ -91,7 +91,8 @@ def test_select_config_always_valid(L):
                             pipes = STREAM_PIPES_LPR4 if c.lanes_per_row == 4 else STREAM_PIPES[c.vecs_per_lane]
                             assert fused or (c.warps_per_cta, c.rows_per_group, c.stages) in pipes
                         elif c.variant == 2:
-                            assert not fused and (F in (1, 2, 4, 8) or (dt == 1 and F == 16))
+                            # one lane per row (4..32-byte rows) or lane groups (64 / 128-byte rows)
+                            assert not fused and (F in (1, 2, 4, 8, 16, 32) or (dt == 1 and F == 64))
                         else:
                             assert c.variant == 1 and 1 <= c.rows_per_group <= 1024
                             assert c.vec_elems in (1, wide) and F % c.vec_elems == 0

@@ -63,11 +63,12 @@ def main():
         allok &= case(E, S, 1, "f32", op, {"variant": 2})          # narrow
         allok &= case(E, S, 4, "bf16", op, {"variant": 2})
         allok &= case(E, S, 128, "f32", op, {"variant": 3})        # stream, selector's pipeline
-        allok &= case(E, S, 16, "f32", op, {"variant": 3})         # stream, 8 agents per warp
+        allok &= case(E, S, 16, "f32", op, {"variant": 3})         # stream, 8 agents per warp (3-D TMA)
+        allok &= case(E, S, 16, "f32", op, {"variant": 2})         # narrow, lane groups of 4
         allok &= case(E, S, 64, "bf16", op, {"variant": 1})        # edge tile + fix-up
         allok &= case(E, S, 12, "f32", op, {"variant": 1})         # scalar-vector edge tile
         allok &= case(E, S, 64, "f32", op, {"variant": 3}, fused=True)
-    allok &= case(E, S, 32, "f32", "sum", {"variant": 3, "warps_per_cta": 8, "rows_per_group": 4, "stages": 0})
+    allok &= case(E, S, 32, "f32", "sum", {"variant": 3, "warps_per_cta": 8, "rows_per_group": 4, "stages": 1})
     allok &= case(E, S, 48, "f32", "sum", {"variant": 1}, fused=True)
     # integer kernels
     L = synth.segment_lengths(E, S, "powerlaw", 11)

@@ -57,7 +57,10 @@ def time_call(fn, reps, flush=None, min_ms=0.0):
 
 
 def make_inputs(E, S, F, dtype, dist, seed, fused=False, V=None, itype=torch.int32):
-    L = synth.segment_lengths(E, S, dist, seed)
+    if dist == "powerlaw15":  # the heavier-tailed degree distribution (Lomax alpha = 1.5)
+        L = synth.segment_lengths(E, S, "powerlaw", seed, alpha=1.5)
+    else:
+        L = synth.segment_lengths(E, S, dist, seed)
     idx = sd.index_from_lengths(L, itype)
     tdt = torch.float32 if dtype == "f32" else torch.bfloat16
     if fused:
@@ -99,13 +102,16 @@ def candidate_configs(E, S, F, dtype, fused, quick=False):
         out.append({"variant": 1, "rows_per_group": R, "ctas_per_sm": c})
     # eligibility from the input alone (not from the current selection)
     esz = 4 if dtype == "f32" else 2
-    narrow_ok = (not fused) and E >= 65536 and (F in (1, 2, 4, 8) or (dtype == "bf16" and F == 16))
+    # one lane per row (4..32-byte rows) or lane groups (64 / 128-byte rows): select.cpp narrow_eligible
+    narrow_ok = (not fused) and E >= 65536 and (F in (1, 2, 4, 8, 16, 32) or (dtype == "bf16" and F == 64))
     shape = stream_lane_shape(F, dtype)
     stream_ok = E >= 65536 and shape is not None and (not fused or shape[1] == 1)
     if narrow_ok:
         out.append({"variant": 2})
     if stream_ok:
-        pipes = [(16, 4, 4), (8, 4, 8), (8, 4, 1)] if shape[0] == 4 else STREAM_PIPES[shape[1]]
+        pipes = [(16, 4, 4), (8, 4, 8), (8, 4, 1)] if shape[0] == 4 else list(STREAM_PIPES[shape[1]])
+        if shape == (16, 1):  # the deeper-stage 256-byte-row pipelines (launch.cuh)
+            pipes += [(16, 12, 2), (16, 8, 3)]
         if fused:  # the gather form's compiled pipelines (launch.cuh launch_stream_gather)
             pipes = [(16, min(6, shape[0]), 4)] + ([(16, 8, 3)] if shape[0] >= 8 else []) + \
                 ([(16, 12, 2)] if shape[0] >= 16 else [])
@@ -208,7 +214,47 @@ def selector_grid_fused():
     return [w for w in selector_grid() if w[6]]
 
 
+# the paper's evaluation datasets (PAPER.md tab:dataset_stats):
+# (nodes, edges) — the base set the r2 grid augments
+PAPER_DATASETS = {"citeseer": (3_327, 9_104), "cora": (2_708, 10_556), "ppi": (2_245, 61_318),
+                  "pubmed": (19_717, 88_648), "amazon_photo": (7_650, 238_162), "flickr": (89_250, 899_756),
+                  "arxiv": (169_343, 1_166_243), "collab": (235_868, 1_285_465), "reddit2": (232_965, 23_213_838)}
+
+
+def selector_grid_r2():
+    """Round-2 performance database: the paper's procedure ("51 valid
+    datasets ... noising and scaling ... 3060 datasets") on synthetic shapes —
+    the Table's nine datasets (plus products- and sweep-sized graphs) SCALED
+    (x1, x16: nodes and edges together, mean degree kept) and NOISED (the
+    degree distribution: Lomax alpha 2 / alpha 1.5 / uniform), at the feature
+    widths of the sweep; bf16, mean/max and the fused form on subsets."""
+    g = []
+    bases = list(PAPER_DATASETS.values()) + [(2_449_029 // 4, 61_859_140 // 4), (1 << 20, 1 << 24)]
+    for (V, E0) in bases:
+        for scale in (1, 16):
+            E, S = E0 * scale, V * scale
+            for dist in ("powerlaw", "powerlaw15", "uniform"):
+                for F in (1, 4, 16, 32, 64, 128, 256):
+                    if E * F * 4 > (3 << 30) or E * F < 4096:
+                        continue
+                    g.append((E, S, F, "f32", dist, "sum", False))
+    for (V, E0) in (PAPER_DATASETS["flickr"], PAPER_DATASETS["arxiv"], PAPER_DATASETS["reddit2"], (1 << 20, 1 << 24)):
+        for F in (1, 8, 16, 32, 64, 128, 256):
+            if E0 * F * 2 <= (3 << 30):
+                g.append((E0, V, F, "bf16", "powerlaw", "sum", False))
+        for op in ("mean", "max"):
+            for F in (1, 16, 64, 128):
+                if E0 * F * 4 <= (3 << 30):
+                    g.append((E0, V, F, "f32", "powerlaw", op, False))
+    for (V, E0) in (PAPER_DATASETS["flickr"], PAPER_DATASETS["arxiv"], PAPER_DATASETS["reddit2"]):
+        for F in (16, 32, 64, 128):
+            for dist in ("powerlaw", "uniform"):
+                g.append((E0, V, F, "f32", dist, "sum", True))
+    return g
+
+
 GRIDS = {
+    "selector_r2": selector_grid_r2(),
     "selector": selector_grid(),
     "selector_fused": selector_grid_fused(),
     "selector_large": selector_grid_large(),
