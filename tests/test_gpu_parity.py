@@ -454,11 +454,12 @@ def test_device_generator_matches_host():
 # ---------------------------------------------------------------- gradients (f3)
 @pytest.mark.parametrize("op", ["sum", "mean", "max"])
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
-def test_segment_reduce_backward(geot, op, dtype):
+@pytest.mark.parametrize("F", [16, 5])  # 16-byte vectors / the scalar path
+def test_segment_reduce_backward(geot, op, dtype, F):
     mode = "int"
-    L, idx, X = make_case(30_000, 4_000, 16, dtype, mode, "gaps", seed=21)
+    L, idx, X = make_case(30_000, 4_000, F, dtype, mode, "gaps", seed=21)
     rng = np.random.default_rng(3)
-    dY = rng.integers(-4, 5, size=(4_000, 16)).astype(np.float32)  # exact in bf16 too
+    dY = rng.integers(-4, 5, size=(4_000, F)).astype(np.float32)  # exact in bf16 too
     ref = oracle.segment_reduce_backward(dY.astype(np.float64), X, idx, op)
     xt = to_torch_vals(X).requires_grad_(True)
     it = torch.from_numpy(idx).to(torch.int32).cuda()
@@ -476,8 +477,9 @@ def test_segment_reduce_backward(geot, op, dtype):
 
 @pytest.mark.parametrize("op", ["sum", "mean"])
 @pytest.mark.parametrize("weighted", [False, True])
-def test_gather_backward_and_sddmm(geot, op, weighted):
-    V, E, S, F = 1_000, 20_000, 800, 32
+@pytest.mark.parametrize("F", [32, 6])  # vector reductions / the scalar path
+def test_gather_backward_and_sddmm(geot, op, weighted, F):
+    V, E, S = 1_000, 20_000, 800
     L = synth.segment_lengths(E, S, "powerlaw", 8)
     dst = synth.lengths_to_index(L, "i64")
     src = synth.src_index(1008, 0, E, V)
