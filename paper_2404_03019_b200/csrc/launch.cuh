@@ -214,6 +214,8 @@ cudaError_t launch_stream(const StreamParams& p, const EdgeTileParams& fix, int 
     GEOT_SSHAPE(16, 1, 16, 12, 2) /* 256-byte rows: deeper stages */
     GEOT_SSHAPE(16, 1, 16, 8, 3)
     GEOT_SSHAPE_V1(32)
+    GEOT_SSHAPE(32, 1, 16, 12, 2) /* 512-byte rows: deeper stages (fewer per-stage overheads) */
+    GEOT_SSHAPE(32, 1, 16, 8, 3)
     GEOT_SSHAPE(32, 2, 16, 3, 4)
     GEOT_SSHAPE(32, 2, 8, 3, 8)
     GEOT_SSHAPE(32, 2, 8, 4, 0)

@@ -88,7 +88,9 @@ def test_select_config_always_valid(L):
                             assert not fused or (c.vecs_per_lane == 1 and (c.warps_per_cta, c.rows_per_group, c.stages)
                                                  in fused_pipes)
                             assert F // wide <= c.lanes_per_row * c.vecs_per_lane
-                            pipes = STREAM_PIPES_LPR4 if c.lanes_per_row == 4 else STREAM_PIPES[c.vecs_per_lane]
+                            pipes = STREAM_PIPES_LPR4 if c.lanes_per_row == 4 else set(STREAM_PIPES[c.vecs_per_lane])
+                            if c.vecs_per_lane == 1 and lpr >= 16:  # deeper stages for 256/512-byte rows
+                                pipes |= {(16, 12, 2), (16, 8, 3)}
                             assert fused or (c.warps_per_cta, c.rows_per_group, c.stages) in pipes
                         elif c.variant == 2:
                             # one lane per row (4..32-byte rows) or lane groups (64 / 128-byte rows)

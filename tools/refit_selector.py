@@ -71,6 +71,30 @@ def label(cfg):
     return (1, int(cfg["rows_per_group"]), 0, 0)
 
 
+class TupleTree:
+    """A decision tree over WHOLE configuration tuples: each distinct tuple
+    (variant, rows_per_group, warps_per_cta, stages) is one class, so every leaf
+    is a configuration that was measured — "the selection of the configuration
+    set in its entirety".  (A per-output multi-output tree can combine
+    the per-output majorities of a leaf into a tuple no sweep ever ran.)"""
+
+    def __init__(self, depth):
+        self.clf = DecisionTreeClassifier(max_depth=depth, random_state=0)
+
+    def fit(self, X, Y):
+        self.tuples = sorted({tuple(int(v) for v in y) for y in Y})
+        ids = {t: i for i, t in enumerate(self.tuples)}
+        self.clf.fit(X, np.array([ids[tuple(int(v) for v in y)] for y in Y]))
+        self.tree_ = self.clf.tree_
+        return self
+
+    def predict(self, X):
+        return np.array([self.tuples[int(c)] for c in self.clf.predict(X)])
+
+    def leaf_tuple(self, node):
+        return list(self.tuples[int(self.clf.classes_[int(np.argmax(self.tree_.value[node][0]))])])
+
+
 def is_test(k):  # deterministic 25 % held-out split
     return int(hashlib.md5(repr(k).encode()).hexdigest(), 16) % 4 == 0
 
@@ -135,7 +159,7 @@ def emit_c(tree, path, provenance):
     def rec(node, depth):
         ind = "    " * depth
         if t.children_left[node] == -1:
-            vals = [int(tree.classes_[o][int(np.argmax(t.value[node][o]))]) for o in range(len(OUTPUTS))]
+            vals = tree.leaf_tuple(node)
             lines.append(f"{ind}out[0] = {vals[0]}; out[1] = {vals[1]}; out[2] = {vals[2]}; out[3] = {vals[3]};")
             return
         f, thr = names[t.feature[node]], float(t.threshold[node])
@@ -155,7 +179,7 @@ def export_json(tree, path):
     nodes = []
     for n in range(t.node_count):
         if t.children_left[n] == -1:
-            vals = [int(tree.classes_[o][int(np.argmax(t.value[n][o]))]) for o in range(len(OUTPUTS))]
+            vals = tree.leaf_tuple(n)
             nodes.append({"leaf": vals})
         else:
             nodes.append({"feature": FEATURES[t.feature[n]], "threshold": float(t.threshold[n]),
@@ -192,7 +216,7 @@ def main():
     X = np.array([features(k) for k in train] + [features(k, False) for k in train])
     Y = tie_aware_labels(by, train, a.tie_tol)
     Y = np.concatenate([Y, Y])
-    tree = DecisionTreeClassifier(max_depth=a.depth, random_state=0).fit(X, Y)
+    tree = TupleTree(a.depth).fit(X, Y)
     q_tr, _ = evaluate(tree, by, train)
     q_te, _ = evaluate(tree, by, test)
     h_tr, _ = evaluate(None, by, train, pick=default_label)
@@ -201,7 +225,7 @@ def main():
     Xa = np.array([features(k) for k in keys] + [features(k, False) for k in keys])
     Ya = tie_aware_labels(by, keys, a.tie_tol)
     Ya = np.concatenate([Ya, Ya])
-    tree_all = DecisionTreeClassifier(max_depth=a.depth, random_state=0).fit(Xa, Ya)
+    tree_all = TupleTree(a.depth).fit(Xa, Ya)
     q_all, _ = evaluate(tree_all, by, keys)
     prov = (f"B200 refit: {len(keys)} workloads ({len(train)} train / {len(test)} held-out), depth {a.depth}, "
             f"tie tol {a.tie_tol:g}, "
@@ -218,7 +242,7 @@ def main():
             f.write("# Selector refit on B200 (H2; PAPER.md §III-C, P:301-315; Fig. 6 analog)\n\n")
             f.write(f"- perf DB: {', '.join(os.path.basename(d) for d in a.db)}; {len(keys)} workloads, "
                     f"{sum(len(v) for v in by.values())} (workload, configuration) timings\n")
-            f.write(f"- tree: multi-output DecisionTreeClassifier, max depth {a.depth}, "
+            f.write(f"- tree: DecisionTreeClassifier over whole configuration tuples, max depth {a.depth}, "
                     f"{tree_all.tree_.n_leaves} leaves, features {FEATURES}, outputs {OUTPUTS}\n")
             f.write("- quality = geomean over workloads of (best measured time / time of the selected "
                     "configuration); 1.0 = always the best\n\n")

@@ -110,7 +110,7 @@ def candidate_configs(E, S, F, dtype, fused, quick=False):
         out.append({"variant": 2})
     if stream_ok:
         pipes = [(16, 4, 4), (8, 4, 8), (8, 4, 1)] if shape[0] == 4 else list(STREAM_PIPES[shape[1]])
-        if shape == (16, 1):  # the deeper-stage 256-byte-row pipelines (launch.cuh)
+        if shape in ((16, 1), (32, 1)):  # the deeper-stage 256/512-byte-row pipelines (launch.cuh)
             pipes += [(16, 12, 2), (16, 8, 3)]
         if fused:  # the gather form's compiled pipelines (launch.cuh launch_stream_gather)
             pipes = [(16, min(6, shape[0]), 4)] + ([(16, 8, 3)] if shape[0] >= 8 else []) + \
@@ -255,6 +255,13 @@ def selector_grid_r2():
 
 GRIDS = {
     "selector_r2": selector_grid_r2(),
+    # the 512-byte-row workloads of the r2 grid again, once the deeper-stage
+    # LPR = 32 pipelines were compiled (tools/merge_perfdb.py replaces them)
+    "selector_r2_lpr32": [w for w in selector_grid_r2() if stream_lane_shape(w[2], w[3]) == (32, 1)],
+    # the widest rows (the sweep's F = 1024; several vectors per lane)
+    "selector_r2_wide": [(E, E // avg, F, dt, "powerlaw", "sum", False)
+                         for F in (512, 1024) for dt in ("f32", "bf16") for E in (1 << 20, 1 << 22, 1 << 24)
+                         for avg in (16, 64) if E * F * (4 if dt == "f32" else 2) <= (68 << 30)],
     "selector": selector_grid(),
     "selector_fused": selector_grid_fused(),
     "selector_large": selector_grid_large(),
