@@ -152,6 +152,13 @@ size_t split_extra_bytes(long long nnz, long long F) {
 }
 
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+// The piece partials go after the reduction's own workspace — and never below
+// its first 256 bytes, the control words of the stream / narrow kernels (ticket,
+// done, epoch, poison), even when this part needs no reduction workspace (a
+// part inside one segment has num_segments = 0 and workspace size 0: placing the
+// partials at offset 0 overwrote the control words of the cached workspace and
+// poisoned every later call on it).
+size_t split_chunk_offset(size_t red) { return align256(red < 256 ? 256 : red); }
 
 }  // namespace
 }  // namespace geot
@@ -180,7 +187,8 @@ geot_status geot_partition_exact(const void* idx, geot_itype itype, int64_t nnz,
 size_t geot_split_workspace_size(int64_t nnz, int64_t num_segments, int64_t F, geot_reduce op, geot_dtype dtype,
                                  geot_itype itype, const geot_config* cfg) {
     if (nnz <= 0 || F < 1) return 0;
-    return align256(geot_workspace_size(nnz, num_segments, F, op, dtype, itype, 0, cfg)) + split_extra_bytes(nnz, F);
+    return split_chunk_offset(geot_workspace_size(nnz, num_segments, F, op, dtype, itype, 0, cfg)) +
+           split_extra_bytes(nnz, F);
 }
 
 geot_status geot_segment_reduce_split(const void* src, const void* idx, int64_t nnz, int64_t seg_base,
@@ -197,14 +205,14 @@ geot_status geot_segment_reduce_split(const void* src, const void* idx, int64_t 
         return GEOT_ERR_INVALID_VALUE;
     }
     const size_t red = nnz > 0 ? geot_workspace_size(nnz, num_segments, F, op, dtype, itype, 0, cfg) : 0;
-    const size_t need = nnz > 0 ? align256(red) + split_extra_bytes(nnz, F) : 0;
+    const size_t need = nnz > 0 ? split_chunk_offset(red) + split_extra_bytes(nnz, F) : 0;
     if (ws_bytes < need) return GEOT_ERR_WORKSPACE_TOO_SMALL;
     if (need > 0 && !workspace) return GEOT_ERR_INVALID_VALUE;
     // the part's own rows (a straddling head's row lies below seg_base: not written)
     geot_status st = geot_segment_reduce_ex(src, idx, nnz, seg_base, num_segments, F, op, dtype, itype, out,
                                             red ? workspace : nullptr, red, cfg, stream);
     if (st != GEOT_OK) return st;
-    float* chunk = reinterpret_cast<float*>(static_cast<unsigned char*>(workspace) + align256(red));
+    float* chunk = reinterpret_cast<float*>(static_cast<unsigned char*>(workspace) + split_chunk_offset(red));
     const long long maxch = (nnz + kSplitChunk - 1) / kSplitChunk;
     const bool ismax = op == GEOT_MAX;
     const int threads = F >= 256 ? 256 : (F >= 128 ? 128 : 64);

@@ -142,3 +142,23 @@ def test_exact_split_two_processes(geot, tmp_path):
     X = synth.values(91, 0, E, F, "f32", "int")
     ref = oracle.segment_reduce(X, idx, S, "sum", nthreads=oracle.default_threads())
     check(np.load(os.path.join(tmp_path, "y.npy")), ref, "sum", "f32", "int", counts=L, what="two-process split")
+
+
+def test_split_part_without_segments_keeps_workspace_healthy(geot):
+    """A part lying inside one segment (num_segments = 0, no reduction workspace)
+    must not write its piece partials over the control words of the cached
+    workspace: the next ticketed (stream / narrow) call would see it poisoned."""
+    E, S, F, P = 90_000, 300, 16, 3
+    L = synth.stress_lengths("single", E, S, seed=P)
+    idx = synth.lengths_to_index(L, "i64")
+    X = synth.values(33, 0, E, F, "f32", "int")
+    y, plans = split_reduce_all_parts(geot, X, idx, S, P, "sum")
+    assert any(pl["s1"] == pl["s0"] for pl in plans)  # the case: a part with no segment of its own
+    assert all(v == 0 for v in geot.geot_workspace_check(repair=False).values())
+    # and a ticketed kernel on the same workspace still writes its output
+    L2 = synth.segment_lengths(200_000, 20_000, "powerlaw", 1)
+    idx2 = synth.lengths_to_index(L2, "i32")
+    X2 = synth.values(5, 0, 200_000, 1, "f32", "int")
+    y2 = geot.geot_segment_reduce(to_torch_vals(X2), torch.from_numpy(idx2).cuda(), 20_000, "sum", cfg={"variant": 2})
+    check(from_torch_vals(y2), oracle.segment_reduce(X2, idx2, 20_000, "sum"), "sum", "f32", "int", counts=L2,
+          what="narrow after a segment-less split part")
