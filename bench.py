@@ -280,10 +280,18 @@ def run_ours(args):
     import torch
     ws, rank, local = dist_env()
     N = ws
+    # GEOT_BENCH_SHARED_GPU=1: every rank on cuda:0 with a gloo process group — a
+    # functional check of the N > 1 path on a one-GPU box (its timings mean nothing)
+    shared = os.environ.get("GEOT_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     if N > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local if N > 1 else 0)
     torch.cuda.set_device(dev)
     import paper_2404_03019_b200 as geot
