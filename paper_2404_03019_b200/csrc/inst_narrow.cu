@@ -65,7 +65,15 @@ static cudaError_t run_narrow_r(NarrowParams p, int nsm, cudaStream_t st) {
     constexpr int KSZ = I64 ? 8 : 4;
     constexpr int LPR = narrow_lpr<T, F>();
     constexpr int NG = 32 / LPR;
-    constexpr int ITEMS = LPR > 1 ? (sizeof(T) == 2 ? 4 : 8) : narrow_items(F, (int)sizeof(T), KSZ);
+// F = 1 with int32 keys: 32 rows per lane (128-byte lane rows of values and of
+// keys, 1 CTA of 8 warps per SM): half the per-row share of the chunk's fixed
+// work (A/B on one box, sweep E = 2^24: fp32 power-law 42.0 -> 38.9 us, uniform
+// 36.9 -> 34.9; bf16 45.1 -> 38.9 / 40.5 -> 34.8)
+#ifndef GEOT_NARROW_F1_ITEMS
+#define GEOT_NARROW_F1_ITEMS 32
+#endif
+    constexpr int ITEMS = LPR > 1 ? (sizeof(T) == 2 ? 4 : 8)
+                                  : ((F == 1 && !I64) ? GEOT_NARROW_F1_ITEMS : narrow_items(F, (int)sizeof(T), KSZ));
     constexpr int LBG = ITEMS * F * (int)sizeof(T), LBK = ITEMS * KSZ;
     auto kern = narrow_kernel<T, F, ITEMS, OP, I64, REP, LPR>;
     const size_t smem = narrow_smem_bytes(LBG, LBK, NG);

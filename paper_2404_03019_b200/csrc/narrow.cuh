@@ -210,8 +210,14 @@ __device__ __forceinline__ void warp_segscan(float (&sv)[F], bool& sf, long long
 // roles of a lane above are played by a group of LPR lanes: group g owns rows
 // g*ITEMS .. of the chunk, each lane its slice of them; the warp pass scans the
 // 32/LPR groups.  F is then the slice width (elements per lane), FR the row.
+// CTAs per SM the kernel is compiled for: 2, or 1 when two rings do not fit
+template <typename T, int FR, int ITEMS, bool I64, int LPR>
+__host__ __device__ constexpr int narrow_min_ctas() {
+    return narrow_smem_bytes(ITEMS * FR * (int)sizeof(T), ITEMS * (I64 ? 8 : 4), 32 / LPR) > 113 * 1024 ? 1 : 2;
+}
+
 template <typename T, int FR, int ITEMS, int OP, bool I64, bool REP = false, int LPR = 1>
-__global__ void __launch_bounds__(kNarrowWarps * 32, 2)
+__global__ void __launch_bounds__(kNarrowWarps * 32, (narrow_min_ctas<T, FR, ITEMS, I64, LPR>()))
     narrow_kernel(const __grid_constant__ CUtensorMap tmv, const __grid_constant__ CUtensorMap tmk,
                   const NarrowParams p) {
     static_assert(FR % LPR == 0 && 32 % LPR == 0, "lane groups");
