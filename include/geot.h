@@ -230,6 +230,31 @@ geot_status geot_segment_reduce_allgather(const void* src, const void* idx, int6
                                           geot_itype itype, void* const* outs, int nouts, void* workspace,
                                           size_t ws_bytes, const geot_config* cfg, cudaStream_t stream);
 
+/* f4, NVLS form (not in the paper, which is single-GPU,
+ * P:338): as geot_segment_reduce_allgather, but the peers' replicas are
+ * reached through ONE multicast address: every finished row (and every
+ * zero-filled empty row) is stored once into local_out with ordinary stores
+ * and once through mc_out with multimem.st, which NVSwitch replicates into
+ * every buffer bound to the multicast object (NVLink SHARP) — one store per
+ * row instead of one per peer.
+ *   local_out  this rank's [total_segments, F] replica (device).
+ *   mc_out     the multicast virtual address of the replicas
+ *              (cuMulticastCreate / cuMulticastBindMem / cuMemMap, or
+ *              torch symmetric memory's multicast_ptr); it maps every rank's
+ *              replica, including this one (its rows are written twice, with
+ *              the same bits).
+ *   Rows of a whole number of 4-byte words and 16-byte aligned buffers only
+ *   (multimem.st has no 2-byte form), and no bf16 edge-tile shape (single
+ *   bf16 elements): else GEOT_ERR_UNSUPPORTED.  NULL pointers, seg_base < 0 ->
+ *   GEOT_ERR_INVALID_VALUE.  Ownership, workspace, stream, ordering and the
+ *   other errors as geot_segment_reduce_allgather.  A plain device address
+ *   passed as mc_out is written with multimem.st and faults: the caller
+ *   checks that multicast is available (it is not on a single-GPU box). */
+geot_status geot_segment_reduce_multicast(const void* src, const void* idx, int64_t nnz, int64_t seg_base,
+                                          int64_t num_segments, int64_t F, geot_reduce op, geot_dtype dtype,
+                                          geot_itype itype, void* local_out, void* mc_out, void* workspace,
+                                          size_t ws_bytes, const geot_config* cfg, cudaStream_t stream);
+
 /* H8: fused gather + segment reduction (P:293 index_segment_reduce):
  *   Y[s,:] = f over { x[src_idx[e], :] : dst_idx[e] == s }.
  *   x        [num_x_rows, F] node features (dtype), device

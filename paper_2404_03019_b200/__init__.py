@@ -205,6 +205,30 @@ def geot_segment_reduce_allgather(src, idx, seg_base, num_segments, outs, op="su
     return outs
 
 
+def geot_segment_reduce_multicast(src, idx, seg_base, num_segments, local_out, mc_ptr, op="sum", cfg=None):
+    """f4, NVLS form: as geot_segment_reduce_allgather, but the peers' replicas are reached
+    through one multicast address `mc_ptr` (an int: e.g. torch symmetric memory's
+    `multicast_ptr`, see shard.open_multicast_replica) written with multimem.st; local_out is
+    this rank's [total_segments, F] replica.  Raises if mc_ptr is 0 (no multicast here)."""
+    dev = _dev(src, idx, local_out)
+    if src.dim() != 2 or idx.dim() != 1 or src.shape[0] != idx.shape[0]:
+        raise ValueError("src must be [nnz, F] and idx [nnz]")
+    E, F = src.shape
+    if (local_out.dim() != 2 or local_out.shape[1] != F or local_out.dtype != src.dtype
+            or local_out.shape[0] < seg_base + num_segments or not local_out.is_contiguous()):
+        raise ValueError("local_out must be a contiguous [total_segments, F] replica with src's dtype")
+    if not mc_ptr:
+        raise ValueError("no multicast address (NVLS unavailable on this system)")
+    ws_n = _L.geot_workspace_size(E, num_segments, F, _op(op), _dt(src), _it(idx), 0, _cfgp(cfg))
+    ws, ws_bytes = _workspace(dev, ws_n)
+    with torch.cuda.device(dev):
+        st = _L.geot_segment_reduce_multicast(_ptr(src), _ptr(idx), E, seg_base, num_segments, F, _op(op), _dt(src),
+                                              _it(idx), _ptr(local_out), ctypes.c_void_p(int(mc_ptr)), _ptr(ws),
+                                              ws_bytes, _cfgp(cfg), _stream(dev))
+    _lib.check(st, "geot_segment_reduce_multicast")
+    return local_out
+
+
 def _num_segments(idx, num_segments):
     if num_segments is not None:
         return int(num_segments)

@@ -10,7 +10,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgeot.so")
+# GEOT_LIB_OVERRIDE: an alternative build of the same library (kernel A/B experiments only)
+LIB_PATH = os.environ.get("GEOT_LIB_OVERRIDE") or os.path.join(_HERE, "libgeot.so")
 
 SUM, MEAN, MAX = 0, 1, 2
 F32, BF16 = 0, 1
@@ -64,6 +65,8 @@ SIGNATURES = {
                                _i32),
     "geot_segment_reduce_allgather": ([_vp, _vp, _i64, _i64, _i64, _i64, _i32, _i32, _i32, ctypes.POINTER(_vp), _i32,
                                        _vp, _sz, _cfgp, _vp], _i32),
+    "geot_segment_reduce_multicast": ([_vp, _vp, _i64, _i64, _i64, _i64, _i32, _i32, _i32, _vp, _vp, _vp, _sz, _cfgp,
+                                       _vp], _i32),
     "geot_gather_segment_reduce": ([_vp, _i64, _vp, _vp, _i64, _i64, _i64, _i32, _i32, _i32, _vp, _vp, _sz, _vp],
                                    _i32),
     "geot_gather_weight_segment_reduce": ([_vp, _i64, _vp, _vp, _vp, _i64, _i64, _i64, _i32, _i32, _vp, _vp, _sz,

@@ -50,6 +50,28 @@ __device__ __forceinline__ void st_vec(uint4* p, uint4 v) { *p = v; }
 __device__ __forceinline__ void st_vec(uint2* p, uint2 v) { *p = v; }
 __device__ __forceinline__ void st_vec(uint32_t* p, uint32_t v) { *p = v; }
 __device__ __forceinline__ void st_vec(uint16_t* p, uint16_t v) { *p = v; }
+// f4, NVLS form: a store through a multicast address (multimem.st; NVSwitch
+// writes it into every replica bound to the multicast object).  4/8/16 bytes —
+// the host rejects rows that are not whole 4-byte words for this form.
+__device__ __forceinline__ void st_mc(uint4* p, uint4 v) {
+    asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+                 "r"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ void st_mc(uint2* p, uint2 v) {
+    asm volatile("multimem.st.relaxed.sys.global.v2.f32 [%0], {%1,%2};" ::"l"(p), "r"(v.x), "r"(v.y) : "memory");
+}
+__device__ __forceinline__ void st_mc(uint32_t* p, uint32_t v) {
+    asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_mc(uint16_t* p, uint16_t v) { *p = v; }  // unreachable (host check)
+template <typename V>
+__device__ __forceinline__ void st_vec_mc(V* p, V v, bool mc) {
+    if (mc)
+        st_mc(p, v);
+    else
+        st_vec(p, v);
+}
 
 __device__ __forceinline__ long long load_index(const void* p, int idx64, long long i) {
     return idx64 ? __ldg(static_cast<const long long*>(p) + i)
@@ -280,8 +302,11 @@ constexpr int kMaxOuts = 8;
 struct OutSet {
     void* ptr[kMaxOuts];
     int n;
+    int mc;  // 1: ptr[1] is a multicast address (NVLS form): stores to it use multimem.st
     long long row_off;
 };
+// destination d of an OutSet: multimem.st for the multicast address
+__device__ __forceinline__ bool out_is_mc(const OutSet& os, int d) { return os.mc && d == 1; }
 
 // Per-tile carry metadata written by the reduction kernel on EVERY call (so
 // the workspace needs no initialisation) and read by the fix-up kernel.

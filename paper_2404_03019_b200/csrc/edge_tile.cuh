@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(256) edge_tile_kernel(const EdgeTileParams p) 
                     float o[VW];
 #pragma unroll
                     for (int q = 0; q < VW; ++q) o[q] = finalize(acc[j][q], p.op, count);
-                    st_vec(reinterpret_cast<Raw*>(rowp + (long long)v * VW), Cv::pack(o));
+                    st_vec_mc(reinterpret_cast<Raw*>(rowp + (long long)v * VW), Cv::pack(o), out_is_mc(p.outs, d));
                 }
             }
         }
@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(256) edge_tile_kernel(const EdgeTileParams p) 
 #pragma unroll
                 for (int j = 0; j < VPL; ++j) {
                     const int v = vec_col(j);
-                    if (v < p.NV) st_vec(reinterpret_cast<Raw*>(rowp + (long long)v * VW), zr);
+                    if (v < p.NV) st_vec_mc(reinterpret_cast<Raw*>(rowp + (long long)v * VW), zr, out_is_mc(p.outs, d));
                 }
             }
     };
@@ -386,8 +386,8 @@ __global__ void __launch_bounds__(256) carry_fixup_kernel(const EdgeTileParams p
         for (int d = 0; d < p.outs.n; ++d) {
             T* orow = static_cast<T*>(p.outs.ptr[d]) + (key - p.outs.row_off) * (long long)p.F;
             if constexpr (sizeof(T) == 4)
-                reinterpret_cast<float*>(orow)[f] = r;
-            else
+                st_vec_mc(reinterpret_cast<uint32_t*>(orow) + f, __float_as_uint(r), out_is_mc(p.outs, d));
+            else  // (no multicast form for bf16 edge tiles: the host rejects it)
                 reinterpret_cast<uint16_t*>(orow)[f] = f2bf_bits(r);
         }
     }

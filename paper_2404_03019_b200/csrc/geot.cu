@@ -385,6 +385,8 @@ static geot_status reduce_common(const void* X, long long V, const void* src_idx
         c.vec_elems = (F % wide == 0) ? wide : 1;  // the edge-tile kernel's vector widths
         select_shape_for_vw(F, dt, &c);
     }
+    // the NVLS form has no 2-byte multicast store: bf16 edge tiles write single elements
+    if (os.mc && dt == GEOT_BF16) return GEOT_ERR_UNSUPPORTED;
     const long long ntiles = ntiles_of(nnz, c);
     const WsLayout L = ws_layout(ntiles, F);
     if (L.total > 0) {
@@ -581,6 +583,26 @@ geot_status geot_segment_reduce_allgather(const void* src, const void* idx, int6
     for (int d = 0; d < nouts; ++d) os.ptr[d] = outs[d];
     os.n = nouts;
     os.row_off = 0;  // every replica holds the full output: rows are global segment ids
+    return reduce_common(src, nnz, nullptr, idx, nullptr, nnz, seg_base, num_segments, F, op, dtype, itype, os,
+                         workspace, ws_bytes, cfg, stream, 0);
+}
+
+geot_status geot_segment_reduce_multicast(const void* src, const void* idx, int64_t nnz, int64_t seg_base,
+                                          int64_t num_segments, int64_t F, geot_reduce op, geot_dtype dtype,
+                                          geot_itype itype, void* local_out, void* mc_out, void* workspace,
+                                          size_t ws_bytes, const geot_config* cfg, cudaStream_t stream) {
+    if (!local_out || !mc_out || seg_base < 0) return GEOT_ERR_INVALID_VALUE;
+    if (check_enums(op, dtype, itype) != GEOT_OK) return GEOT_ERR_INVALID_VALUE;
+    const int esz = dtype == GEOT_F32 ? 4 : 2;
+    // multimem.st moves whole 4/8/16-byte words: rows of whole words, word-aligned buffers
+    if ((F * esz) % 4 != 0 || (reinterpret_cast<uintptr_t>(local_out) | reinterpret_cast<uintptr_t>(mc_out)) % 16 != 0)
+        return GEOT_ERR_UNSUPPORTED;
+    OutSet os{};
+    os.ptr[0] = local_out;
+    os.ptr[1] = mc_out;
+    os.n = 2;
+    os.mc = 1;
+    os.row_off = 0;  // full-output replicas: rows are global segment ids
     return reduce_common(src, nnz, nullptr, idx, nullptr, nnz, seg_base, num_segments, F, op, dtype, itype, os,
                          workspace, ws_bytes, cfg, stream, 0);
 }

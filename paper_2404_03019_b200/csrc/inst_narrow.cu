@@ -75,16 +75,24 @@ static cudaError_t run_narrow_r(NarrowParams p, int nsm, cudaStream_t st) {
     constexpr int ITEMS = LPR > 1 ? (sizeof(T) == 2 ? 4 : 8)
                                   : ((F == 1 && !I64) ? GEOT_NARROW_F1_ITEMS : narrow_items(F, (int)sizeof(T), KSZ));
     constexpr int LBG = ITEMS * F * (int)sizeof(T), LBK = ITEMS * KSZ;
-    auto kern = narrow_kernel<T, F, ITEMS, OP, I64, REP, LPR>;
-    const size_t smem = narrow_smem_bytes(LBG, LBK, NG);
-    int occ = cached_occupancy(kern, kNarrowWarps * 32, smem);
+#ifndef GEOT_NARROW_F1_WARPS
+#define GEOT_NARROW_F1_WARPS 12
+#endif
+    // fp32 F = 1 at 32 rows per lane: the 8 KB stages hold one CTA per SM, so the
+    // CTA takes 12 warps (192 KB ring, 156 registers): the kernel is latency-bound
+    // (issue-active 49 % at 8 warps), A/B on one box: power-law 36.9 -> 35.2 us,
+    // uniform 33.4 -> 33.1 (8 warps with a third stage instead: 37.0 -> 37.6)
+    constexpr int NW = (F == 1 && sizeof(T) == 4 && ITEMS == 32 && LPR == 1) ? GEOT_NARROW_F1_WARPS : kNarrowWarps;
+    auto kern = narrow_kernel<T, F, ITEMS, OP, I64, REP, LPR, NW>;
+    const size_t smem = narrow_smem_bytes(LBG, LBK, NG, NW);
+    int occ = cached_occupancy(kern, NW * 32, smem);
     if (occ <= 0) return cudaErrorInvalidConfiguration;
     // every agent (warp) must own at least one chunk of NG*ITEMS rows
     long long grid = (long long)nsm * occ;
     const long long max_agents = p.E / ((long long)NG * ITEMS);
-    if (grid * kNarrowWarps > max_agents) grid = max_agents / kNarrowWarps;
+    if (grid * NW > max_agents) grid = max_agents / NW;
     if (grid < 1) return cudaErrorNotSupported;
-    p.NA = grid * kNarrowWarps;
+    p.NA = grid * NW;
     // whole lane rows only: the tail (< one lane row) is read directly
     CUtensorMap tmv, tmk;
     memset(&tmv, 0, sizeof(tmv));
@@ -94,7 +102,7 @@ static cudaError_t run_narrow_r(NarrowParams p, int nsm, cudaStream_t st) {
                 ? 1
                 : 0;
     if (g_prof_before) cudaEventRecord(g_prof_before, st);
-    kern<<<(unsigned)grid, kNarrowWarps * 32, smem, st>>>(tmv, tmk, p);
+    kern<<<(unsigned)grid, NW * 32, smem, st>>>(tmv, tmk, p);
     if (g_prof_after) cudaEventRecord(g_prof_after, st);
     g_prof_before = g_prof_after = nullptr;
     cudaError_t e = cudaGetLastError();
@@ -136,7 +144,7 @@ static cudaError_t launch_narrow_t(const NarrowParams& p, int F, bool i64, int n
 }
 
 // Agents the launcher will use (carry slots); 0 = not applicable.
-long long narrow_agents_max(int nsm) { return (long long)nsm * 8 * kNarrowWarps; }
+long long narrow_agents_max(int nsm) { return (long long)nsm * 8 * kNarrowWarps; }  // >= every NW * CTAs/SM
 
 cudaError_t launch_narrow(const NarrowParams& p, int F, bool bf16, bool ismax, bool i64, int nsm, cudaStream_t st) {
     (void)ismax;  // p.op carries the op

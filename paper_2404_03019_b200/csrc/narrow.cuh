@@ -69,14 +69,16 @@ __host__ __device__ constexpr int narrow_area(int lb, int ng = 32) { return ((ng
 __host__ __device__ constexpr int narrow_stage_bytes(int lbv, int lbk, int ng = 32) {
     return narrow_area(lbv, ng) + narrow_area(lbk, ng);
 }
-// ring depth: 3 stages of <= 4 KB, else 2 (two 8-warp CTAs per SM fit either way)
+// ring depth: 3 stages of <= 4 KB, else 2 (two 8-warp CTAs per SM fit either way;
+// F = 1 at 32 rows per lane, 8 KB stages, 1 CTA/SM: a third stage measured
+// 37.0 -> 37.6 us, the kernel is not bound by bytes in flight)
 __host__ __device__ constexpr int narrow_stages(int lbv, int lbk, int ng = 32) {
     return narrow_stage_bytes(lbv, lbk, ng) <= 4096 ? 3 : 2;
 }
-__host__ __device__ constexpr size_t narrow_smem_bytes(int lbv, int lbk, int ng = 32) {
-    return (size_t)kNarrowWarps * narrow_stages(lbv, lbk, ng) * narrow_stage_bytes(lbv, lbk, ng)  // rings
-           + (size_t)kNarrowWarps * narrow_stages(lbv, lbk, ng) * 8                              // mbarriers
-           + 1024;                                                                       // alignment slack
+__host__ __device__ constexpr size_t narrow_smem_bytes(int lbv, int lbk, int ng = 32, int nw = kNarrowWarps) {
+    return (size_t)nw * narrow_stages(lbv, lbk, ng) * narrow_stage_bytes(lbv, lbk, ng)  // rings
+           + (size_t)nw * narrow_stages(lbv, lbk, ng) * 8                              // mbarriers
+           + 1024;                                                             // alignment slack
 }
 
 // physical offset of logical byte o of a tile written by TMA with the swizzle
@@ -137,33 +139,37 @@ __device__ __forceinline__ float ld_elem(const T* p) {
 
 // one output row of F elements from fp32 values (vector stores when they fit)
 template <typename T, int F>
-__device__ __forceinline__ void st_row(T* row, const float (&v)[F]) {
+__device__ __forceinline__ void st_row(T* row, const float (&v)[F], bool mc = false) {
+    // (mc: the multicast destination of the f4 NVLS form, multimem.st)
     if constexpr (sizeof(T) == 4) {
         if constexpr (F % 4 == 0) {
 #pragma unroll
             for (int f = 0; f < F; f += 4)
-                *reinterpret_cast<float4*>(row + f) = make_float4(v[f], v[f + 1], v[f + 2], v[f + 3]);
+                st_vec_mc(reinterpret_cast<uint4*>(row + f),
+                          make_uint4(__float_as_uint(v[f]), __float_as_uint(v[f + 1]), __float_as_uint(v[f + 2]),
+                                     __float_as_uint(v[f + 3])),
+                          mc);
         } else if constexpr (F == 2) {
-            *reinterpret_cast<float2*>(row) = make_float2(v[0], v[1]);
+            st_vec_mc(reinterpret_cast<uint2*>(row), make_uint2(__float_as_uint(v[0]), __float_as_uint(v[1])), mc);
         } else {
-            *reinterpret_cast<float*>(row) = v[0];
+            st_vec_mc(reinterpret_cast<uint32_t*>(row), __float_as_uint(v[0]), mc);
         }
     } else {
         if constexpr (F == 1) {
-            *reinterpret_cast<uint16_t*>(row) = f2bf_bits(v[0]);
+            *reinterpret_cast<uint16_t*>(row) = f2bf_bits(v[0]);  // (no multicast form: 2-byte rows)
         } else {
             uint32_t w[F / 2];
 #pragma unroll
             for (int i = 0; i < F / 2; ++i)
                 w[i] = (uint32_t)f2bf_bits(v[2 * i]) | ((uint32_t)f2bf_bits(v[2 * i + 1]) << 16);
             if constexpr (F == 2) {
-                *reinterpret_cast<uint32_t*>(row) = w[0];
+                st_vec_mc(reinterpret_cast<uint32_t*>(row), w[0], mc);
             } else if constexpr (F == 4) {
-                *reinterpret_cast<uint2*>(row) = make_uint2(w[0], w[1]);
+                st_vec_mc(reinterpret_cast<uint2*>(row), make_uint2(w[0], w[1]), mc);
             } else {
 #pragma unroll
                 for (int i = 0; i < F / 2; i += 4)
-                    *reinterpret_cast<uint4*>(row + 2 * i) = make_uint4(w[i], w[i + 1], w[i + 2], w[i + 3]);
+                    st_vec_mc(reinterpret_cast<uint4*>(row + 2 * i), make_uint4(w[i], w[i + 1], w[i + 2], w[i + 3]), mc);
             }
         }
     }
@@ -211,13 +217,14 @@ __device__ __forceinline__ void warp_segscan(float (&sv)[F], bool& sf, long long
 // g*ITEMS .. of the chunk, each lane its slice of them; the warp pass scans the
 // 32/LPR groups.  F is then the slice width (elements per lane), FR the row.
 // CTAs per SM the kernel is compiled for: 2, or 1 when two rings do not fit
-template <typename T, int FR, int ITEMS, bool I64, int LPR>
+template <typename T, int FR, int ITEMS, bool I64, int LPR, int NW = kNarrowWarps>
 __host__ __device__ constexpr int narrow_min_ctas() {
-    return narrow_smem_bytes(ITEMS * FR * (int)sizeof(T), ITEMS * (I64 ? 8 : 4), 32 / LPR) > 113 * 1024 ? 1 : 2;
+    return narrow_smem_bytes(ITEMS * FR * (int)sizeof(T), ITEMS * (I64 ? 8 : 4), 32 / LPR, NW) > 113 * 1024 ? 1 : 2;
 }
 
-template <typename T, int FR, int ITEMS, int OP, bool I64, bool REP = false, int LPR = 1>
-__global__ void __launch_bounds__(kNarrowWarps * 32, (narrow_min_ctas<T, FR, ITEMS, I64, LPR>()))
+// NW warps (agents) per CTA: 8, or 12 where one CTA per SM holds the ring anyway
+template <typename T, int FR, int ITEMS, int OP, bool I64, bool REP = false, int LPR = 1, int NW = kNarrowWarps>
+__global__ void __launch_bounds__(NW * 32, (narrow_min_ctas<T, FR, ITEMS, I64, LPR, NW>()))
     narrow_kernel(const __grid_constant__ CUtensorMap tmv, const __grid_constant__ CUtensorMap tmk,
                   const NarrowParams p) {
     static_assert(FR % LPR == 0 && 32 % LPR == 0, "lane groups");
@@ -249,7 +256,7 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, (narrow_min_ctas<T, FR, ITE
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int grp = lane / LPR, li = lane % LPR;  // row-owner group, slice within the row
     const uint32_t ring = smem_u32(smem_raw) + (uint32_t)(warp * NS * STAGE);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + (size_t)kNarrowWarps * NS * STAGE) + warp * NS;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + (size_t)NW * NS * STAGE) + warp * NS;
 
     const T* __restrict__ X = static_cast<const T*>(p.X);
     const KT* __restrict__ I = static_cast<const KT*>(p.idx);
@@ -265,7 +272,7 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, (narrow_min_ctas<T, FR, ITE
         return;
     }
     const unsigned long long pub = s_epoch + 1;
-    const long long a = (long long)s_ticket * kNarrowWarps + warp;
+    const long long a = (long long)s_ticket * NW + warp;
     auto agent_lo = [&](long long x) -> long long {
         if (x >= p.NA) return E;
         return ((x * E) / p.NA) / ITEMS * ITEMS;
@@ -303,7 +310,8 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, (narrow_min_ctas<T, FR, ITE
         if constexpr (REP) {
             for (int d = 0; d < p.outs.n; ++d)
                 for (long long r = r0; r < r1; ++r)
-                    st_row<T, F>(static_cast<T*>(p.outs.ptr[d]) + (r - p.outs.row_off) * FR + li * F, z);
+                    st_row<T, F>(static_cast<T*>(p.outs.ptr[d]) + (r - p.outs.row_off) * FR + li * F, z,
+                                 out_is_mc(p.outs, d));
         } else {
             for (long long r = r0; r < r1; ++r) st_row<T, F>(out0 + (r - seg_lo) * FR, z);
         }
@@ -330,7 +338,7 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, (narrow_min_ctas<T, FR, ITE
             if constexpr (REP)  // replicas (f4): global row index
                 for (int d = 1; d < p.outs.n; ++d)
                     st_row<T, F>(static_cast<T*>(p.outs.ptr[d]) + ((long long)rel + seg_lo - p.outs.row_off) * FR + li * F,
-                                 o);
+                                 o, out_is_mc(p.outs, d));
         }
     };
 
@@ -429,10 +437,31 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, (narrow_min_ctas<T, FR, ITE
         unsigned hm = (nv > 0 && k[0] != kp) ? 1u : 0u;
 #pragma unroll
         for (int i = 1; i < ITEMS; ++i) hm |= (unsigned)(k[i] != k[i - 1]) << i;  // padding repeats the last key
+#ifndef GEOT_NARROW_FMA_CHAIN
+#define GEOT_NARROW_FMA_CHAIN 0
+#endif
 #pragma unroll
         for (int i = 1; i < ITEMS; ++i) {
             const bool h = (hm >> i) & 1u;
-            if constexpr (OP != OP_MAX && F % 2 == 0) {  // packed fp32x2 adds (FADD2)
+            if constexpr (OP != OP_MAX && GEOT_NARROW_FMA_CHAIN) {
+                // the restart folded into the add: acc[i] = m * acc[i-1] + acc[i] with
+                // m = 0 at a head, 1 elsewhere (fma(1, a, x) rounds exactly like a + x,
+                // fma(0, a, x) = x for finite a) — ONE dependent instruction per item
+                // on the lane's chain instead of an add and a select
+                const float m = h ? 0.f : 1.f;
+                if constexpr (F % 2 == 0) {
+#pragma unroll
+                    for (int f = 0; f < F; f += 2) {
+                        const float2 t = __ffma2_rn(make_float2(m, m), make_float2(acc[i - 1][f], acc[i - 1][f + 1]),
+                                                    make_float2(acc[i][f], acc[i][f + 1]));
+                        acc[i][f] = t.x;
+                        acc[i][f + 1] = t.y;
+                    }
+                } else {
+#pragma unroll
+                    for (int f = 0; f < F; ++f) acc[i][f] = __fmaf_rn(m, acc[i - 1][f], acc[i][f]);
+                }
+            } else if constexpr (OP != OP_MAX && F % 2 == 0) {  // packed fp32x2 adds (FADD2)
 #pragma unroll
                 for (int f = 0; f < F; f += 2) {
                     const float2 t = __fadd2_rn(make_float2(acc[i - 1][f], acc[i - 1][f + 1]),
@@ -650,7 +679,8 @@ __global__ void __launch_bounds__(kNarrowWarps * 32, (narrow_min_ctas<T, FR, ITE
             if constexpr (REP) {
                 for (int d = 0; d < p.outs.n; ++d) {
                     U* const g = reinterpret_cast<U*>(static_cast<T*>(p.outs.ptr[d]) + (lo - p.outs.row_off) * FR);
-                    for (int u = lane; u < nunits; u += 32) g[u] = wu[u];
+                    const bool mc = out_is_mc(p.outs, d);
+                    for (int u = lane; u < nunits; u += 32) st_vec_mc(g + u, wu[u], mc);
                 }
             } else {
                 U* const g = reinterpret_cast<U*>(out0 - li * F + (lo - seg_lo) * FR);

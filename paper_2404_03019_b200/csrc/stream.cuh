@@ -85,6 +85,23 @@ __device__ __forceinline__ bool wait_flag_or_poison(const unsigned long long* p,
     return true;
 }
 
+#ifdef GEOT_TRACE
+// experiments only (-DGEOT_TRACE, tools/trace_stream.py): per-CTA start / end
+// and per-agent loop-end %globaltimer stamps, read back by geot_debug_trace
+__device__ unsigned long long g_trace_cta[4096 * 4];
+__device__ unsigned long long g_trace_agent[65536];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ unsigned smid() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(r));
+    return r;
+}
+#endif
+
 // CTA end: the last CTA out re-arms ticket / done and advances the epoch.
 __device__ __forceinline__ void retire_cta(StreamCtrl* ctrl) {
     __syncthreads();
@@ -214,6 +231,12 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2)
         return;
     }
     const unsigned long long pub = s_epoch + 1;  // "published in this call" flag value
+#ifdef GEOT_TRACE
+    if (threadIdx.x == 0 && s_ticket < 4096) {
+        g_trace_cta[s_ticket * 4 + 0] = gtimer();
+        g_trace_cta[s_ticket * 4 + 2] = smid();
+    }
+#endif
 
     // agent ranges.  4+ agents per warp (EQL): L rows each (L = ceil(E / NA)
     // rounded up to RS), so every stage of a full agent holds RS rows and the G
@@ -422,7 +445,7 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2)
             for (int d = 1; d < p.outs.n; ++d) {
                 T* rp = static_cast<T*>(p.outs.ptr[d]) + (key - p.outs.row_off) * (long long)F;
                 for (int j = 0; j < VPL; ++j)
-                    if (vec_col(j) < p.NV) st_vec(reinterpret_cast<Raw*>(rp + vec_col(j) * VW), packed[j]);
+                    if (vec_col(j) < p.NV) st_vec_mc(reinterpret_cast<Raw*>(rp + vec_col(j) * VW), packed[j], out_is_mc(p.outs, d));
             }
         }
     };
@@ -446,7 +469,7 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2)
                 for (int d = 1; d < p.outs.n; ++d) {
                     T* rp = static_cast<T*>(p.outs.ptr[d]) + (key - p.outs.row_off) * (long long)F;
                     for (int j = 0; j < VPL; ++j)
-                        if (vec_col(j) < p.NV) st_vec(reinterpret_cast<Raw*>(rp + vec_col(j) * VW), packed[j]);
+                        if (vec_col(j) < p.NV) st_vec_mc(reinterpret_cast<Raw*>(rp + vec_col(j) * VW), packed[j], out_is_mc(p.outs, d));
                 }
         }
     };
@@ -470,7 +493,7 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2)
                 for (long long r = r0; r < r1; ++r) {
                     T* rp = static_cast<T*>(p.outs.ptr[d]) + (r - p.outs.row_off) * (long long)F;
                     for (int j = 0; j < VPL; ++j)
-                        if (vec_col(j) < p.NV) st_vec(reinterpret_cast<Raw*>(rp + vec_col(j) * VW), zr);
+                        if (vec_col(j) < p.NV) st_vec_mc(reinterpret_cast<Raw*>(rp + vec_col(j) * VW), zr, out_is_mc(p.outs, d));
                 }
             }
         }
@@ -708,7 +731,7 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2)
                             for (int d = 1; d < p.outs.n; ++d) {
                                 T* rp = static_cast<T*>(p.outs.ptr[d]) +
                                         ((long long)crel + seg_lo - p.outs.row_off) * (long long)F + li * VW;
-                                st_vec(reinterpret_cast<Raw*>(rp), pk);
+                                st_vec_mc(reinterpret_cast<Raw*>(rp), pk, out_is_mc(p.outs, d));
                             }
                     }
                 }
@@ -866,6 +889,9 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2)
         }
     }
 
+#ifdef GEOT_TRACE
+    if (li == 0 && a < 65536) g_trace_agent[a] = gtimer();
+#endif
     // ---- agent end: publish the carries later agents need (H5) ...
     sync_acc();
     if (nrows > 0) {
@@ -941,6 +967,10 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2)
         }
     }
     // ---- last CTA out re-arms the control words for the next call
+#ifdef GEOT_TRACE
+    __syncthreads();
+    if (threadIdx.x == 0 && s_ticket < 4096) g_trace_cta[s_ticket * 4 + 1] = gtimer();
+#endif
     retire_cta(p.ctrl);
 }
 

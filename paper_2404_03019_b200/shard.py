@@ -84,6 +84,19 @@ def open_peer_replicas(local_full, group=None):
     return [local_full if r == me else fn(*args) for r, (fn, args) in enumerate(objs)]
 
 
+def open_multicast_replica(shape, dtype, group=None):
+    """f4 NVLS plumbing: a full-output replica in torch symmetric memory, rendezvoused
+    across the group.  Returns (replica, multicast_ptr); multicast_ptr is 0 when the
+    system has no NVLS multicast (e.g. one GPU, or no fabric manager) — then use
+    open_peer_replicas + geot_segment_reduce_allgather (P unicast stores) instead."""
+    import torch
+    import torch.distributed as dist
+    import torch.distributed._symmetric_memory as symm_mem
+    t = symm_mem.empty(tuple(shape), dtype=dtype, device=torch.device("cuda", torch.cuda.current_device()))
+    g = group if group is not None else dist.group.WORLD
+    h = symm_mem.rendezvous(t, g.group_name)
+    return t, int(getattr(h, "multicast_ptr", 0) or 0)
+
 
 # ---------------------------------------------------------------------------
 # f4 "Alternative partition": the exact edge split with a one-step exchange

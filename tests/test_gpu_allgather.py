@@ -118,3 +118,74 @@ def test_allgather_two_ranks_cuda_ipc(geot):
     import torch.multiprocessing as mp
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     mp.spawn(_ipc_worker, args=(2, _free_port(), 250_000, 18_000, 64), nprocs=2, join=True)
+
+
+# ---------------------------------------------------------------------------
+# f4, NVLS form (geot_segment_reduce_multicast): rows stored through one
+# multicast address with multimem.st.  Needs NVSwitch multicast (a multi-GPU
+# NVLink node with the fabric manager): on a box without it, torch symmetric
+# memory hands out multicast_ptr = 0 and the bit-exact check is skipped with
+# that reason; the argument contract is checked everywhere.
+def test_multicast_rejects_bad_args(geot):
+    x = torch.ones((10, 4), device="cuda")
+    i = torch.zeros(10, dtype=torch.int32, device="cuda")
+    full = torch.zeros((1, 4), device="cuda")
+    with pytest.raises(ValueError):  # no multicast address
+        geot.geot_segment_reduce_multicast(x, i, 0, 1, full, 0, "sum")
+    with pytest.raises(ValueError):  # replica shape
+        geot.geot_segment_reduce_multicast(x, i, 0, 1, torch.zeros((1, 3), device="cuda"), 1 << 40, "sum")
+    xb = torch.ones((10, 1), device="cuda", dtype=torch.bfloat16)  # 2-byte rows: no multimem form
+    with pytest.raises(RuntimeError, match="UNSUPPORTED"):
+        geot.geot_segment_reduce_multicast(xb, i, 0, 1, torch.zeros((1, 1), device="cuda", dtype=torch.bfloat16),
+                                           1 << 40, "sum")
+
+
+def _mc_worker(rank, world, port, E, S, F, op, q):
+    import torch.distributed as dist
+
+    import paper_2404_03019_b200 as g
+    from paper_2404_03019_b200 import shard
+    os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    try:
+        torch.cuda.set_device(rank)
+        try:
+            rep, mc = shard.open_multicast_replica((S, F), torch.float32)
+        except Exception as ex:  # noqa: BLE001  (no symmetric-memory backend here)
+            q.put(("skip", f"symmetric memory unavailable: {str(ex)[:120]}"))
+            return
+        if not mc:
+            q.put(("skip", "NVLS multicast unavailable on this system (multicast_ptr = 0)"))
+            return
+        idx, X = _case(E, S, F, "gaps", 31)
+        it = torch.from_numpy(idx).to(torch.int32).cuda()
+        sb, eb = g.geot_partition(it, S, world)
+        sb, eb = sb.cpu().tolist(), eb.cpu().tolist()
+        xt = torch.from_numpy(X).cuda()
+        rep.fill_(-5.0)
+        torch.cuda.synchronize()
+        dist.barrier()
+        g.geot_segment_reduce_multicast(xt[eb[rank]:eb[rank + 1]], it[eb[rank]:eb[rank + 1]], sb[rank],
+                                        sb[rank + 1] - sb[rank], rep, mc, op)
+        torch.cuda.synchronize()
+        dist.barrier()
+        ref = oracle.segment_reduce(X, idx, S, op)
+        ok = np.array_equal(rep.cpu().numpy().view(np.uint8), ref.rounded.view(np.uint8))
+        q.put(("ok" if ok else "fail", f"rank {rank}"))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("F,op", [(128, "sum"), (4, "max"), (3, "mean")])
+def test_multicast_replicas_bit_exact(geot, F, op):
+    import torch.multiprocessing as mp
+    world = torch.cuda.device_count()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    mp.start_processes(_mc_worker, args=(world, _free_port(), 220_000, 16_000, F, op, q), nprocs=world, join=True,
+                       start_method="spawn")
+    res = [q.get() for _ in range(world)]
+    if any(r[0] == "skip" for r in res):
+        pytest.skip(next(r[1] for r in res if r[0] == "skip"))
+    assert all(r[0] == "ok" for r in res), res
