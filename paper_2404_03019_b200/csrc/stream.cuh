@@ -309,6 +309,7 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2)
 
     const bool col_ok0 = li < p.NV;  // (fused forms: one 16-byte vector per lane)
     const unsigned long long xrows = (unsigned long long)p.V;
+    const unsigned xrows32 = p.V < 0xFFFFFFFFLL ? (unsigned)p.V : 0xFFFFFFFFu;
     const unsigned xrow_bytes = (unsigned)p.row_bytes;
     const unsigned char* xlane = reinterpret_cast<const unsigned char*>(X) + li * 16;  // this lane's column
     // fused forms: the src ids of stage s + NS are cp.async-loaded into the id
@@ -332,24 +333,30 @@ __global__ void __launch_bounds__(W * 32, NS > 0 ? 1 : 2)
             // gather: lane li copies its 16-byte slices of each of the stage's rows
             // x[src] (cp.async, L2 only); the ids come from this buffer's id slots
             long long cl = e_hi - (e_lo + (long long)s * RS);
-            const int c = cl < 0 ? 0 : (cl > RS ? RS : (int)cl);
+            int c = cl < 0 ? 0 : (cl > RS ? RS : (int)cl);
+            c = col_ok0 ? c : 0;
+            asm volatile("" : "+r"(c));  // a 32-bit row count (no 64-bit compare per row)
             const unsigned long long* ids = sring + (b * G + gi) * RS;
             const uint32_t gbase = smem_u32(wbuf) + (uint32_t)(b * stage_bytes + gi * RS * row_bytes + li * 16);
 #pragma unroll
             for (int r = 0; r < RS; ++r) {
-                if (r < c && col_ok0) {
+                if (r < c) {
                     const unsigned long long raw = ids[r];  // broadcast within the group
-                    bool ok;
-                    size_t off;  // byte offset of row src in x
                     if constexpr (SRC64) {
-                        ok = raw < xrows;
-                        off = (size_t)(ok ? raw : 0ull) * xrow_bytes;
+                        const bool ok = raw < xrows;
+                        const size_t off = (size_t)(ok ? raw : 0ull) * xrow_bytes;  // byte offset of row src in x
+                        cp_async_16_zfill(gbase + (uint32_t)(r * row_bytes), xlane + off, ok ? 16u : 0u);
                     } else {
+                        // int32 ids (V < 2^31): the row address is ONE wide multiply-add
                         const unsigned sid = (unsigned)raw;
-                        ok = sid < (unsigned)xrows;  // V < 2^31 with int32 ids
-                        off = (size_t)(ok ? sid : 0u) * xrow_bytes;
+                        const bool ok = sid < xrows32;
+                        unsigned long long addr;
+                        asm("mad.wide.u32 %0, %1, %2, %3;"
+                            : "=l"(addr)
+                            : "r"(ok ? sid : 0u), "r"(xrow_bytes), "l"(reinterpret_cast<unsigned long long>(xlane)));
+                        cp_async_16_zfill(gbase + (uint32_t)(r * row_bytes), reinterpret_cast<const void*>(addr),
+                                          ok ? 16u : 0u);
                     }
-                    cp_async_16_zfill(gbase + (uint32_t)(r * row_bytes), xlane + off, ok ? 16u : 0u);
                 }
             }
             __syncwarp();  // every lane has read the id slots before they are refilled
