@@ -29,10 +29,14 @@ def sample_segments(L, E, rng, n_random=4000, n_long=50):
     bounds = synth.lengths_to_bounds(L)
     picks = set(rng.choice(S, size=min(n_random, S), replace=False).tolist())
     picks |= set(np.argsort(L)[-n_long:].tolist())
-    for NA in (1184, 2368, 4736, 9472):  # agent splits of the narrow kernel (ITEMS-aligned k*E/NA)
-        for k in range(1, NA):
-            e = (k * E) // NA
-            picks.add(int(np.searchsorted(bounds, e, side="right") - 1))
+    nsm = torch.cuda.get_device_properties(0).multi_processor_count if torch.cuda.is_available() else 148
+    # agent splits of the narrow kernel: NA = SMs x CTAs/SM x warps (8, or 12 for fp32 F=1),
+    # boundaries ((k*E)/NA) rounded down to ITEMS rows (narrow.cuh agent_lo)
+    for NA in sorted({nsm * c * w for c in (1, 2) for w in (8, 12)} | {nsm * 32, nsm * 64}):
+        k = np.arange(1, NA, dtype=np.int64)
+        for items in (1, 8, 16, 32):
+            e = (k * E) // NA // items * items
+            picks.update((np.searchsorted(bounds, e, side="right") - 1).tolist())
     for NA in (2368, 4736, 9472, 18944):  # stream kernel: L = ceil(E/NA) rounded up to RS rows per agent
         for RS in (4, 6, 12):
             Lr = (-(-E // NA) + RS - 1) // RS * RS
