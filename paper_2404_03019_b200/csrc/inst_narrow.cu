@@ -69,11 +69,19 @@ static cudaError_t run_narrow_r(NarrowParams p, int nsm, cudaStream_t st) {
 // keys, 1 CTA of 8 warps per SM): half the per-row share of the chunk's fixed
 // work (A/B on one box, sweep E = 2^24: fp32 power-law 42.0 -> 38.9 us, uniform
 // 36.9 -> 34.9; bf16 45.1 -> 38.9 / 40.5 -> 34.8)
+// F = 1 with int64 keys: 16 rows per lane (128-byte lane rows of keys; the
+// generic rule caps keys at 64 bytes per lane): A/B on one box, E = 2^24 fp32
+// power-law 55.0 -> 41.9 us, uniform 55.6 -> 43.3 us
+#ifndef GEOT_NARROW_F1_I64_ITEMS
+#define GEOT_NARROW_F1_I64_ITEMS 16
+#endif
 #ifndef GEOT_NARROW_F1_ITEMS
 #define GEOT_NARROW_F1_ITEMS 32
 #endif
     constexpr int ITEMS = LPR > 1 ? (sizeof(T) == 2 ? 4 : 8)
-                                  : ((F == 1 && !I64) ? GEOT_NARROW_F1_ITEMS : narrow_items(F, (int)sizeof(T), KSZ));
+                                  : ((F == 1 && !I64) ? GEOT_NARROW_F1_ITEMS
+                                     : (F == 1 && I64)  ? GEOT_NARROW_F1_I64_ITEMS
+                                                        : narrow_items(F, (int)sizeof(T), KSZ));
     constexpr int LBG = ITEMS * F * (int)sizeof(T), LBK = ITEMS * KSZ;
 #ifndef GEOT_NARROW_F1_WARPS
 #define GEOT_NARROW_F1_WARPS 12
